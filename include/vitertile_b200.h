@@ -1,0 +1,115 @@
+/*
+ * vitertile_b200 — C ABI of the B200-native framed Viterbi decoder.
+ *
+ * Drop-in boundary for the reference's decode hot path.  The reference
+ * (vitertile 0.1.0, pure Python) has no FFI; its operator boundary is the
+ * string dispatch decoder in {"reference","matrix"} plus DecoderConfig
+ * (pkg/src/vitertile/framing.py:86-93,111; channel.py:102-110; cli.py:93-97).
+ * Every entry point below replaces one reference function on that path:
+ *
+ *   vt_decode_stream        <- framing.decode_stream / _decode_windows
+ *                              (framing.py:86-141) with decoder="reference"
+ *                              (reference.decode_batch, reference.py:194-206)
+ *   vt_decode_stream_range  <- the same, restricted to windows [w0, w1) of a
+ *                              stage sub-range held in device memory (lets the
+ *                              host pipeline H2D copies and shard across GPUs)
+ *   vt_decode_frames        <- reference.decode_batch (reference.py:194-206):
+ *                              F independent frames of N stages, zero initial
+ *                              metrics, per-frame final metric
+ *   vt_decode_stream_host   <- decode_stream called with HOST buffers (the
+ *                              CLI path, cli.py:133-175): H2D, decode, D2H
+ *
+ * Conventions (all calls):
+ *   - Plain pointers and sizes; no allocation inside a call (the caller passes
+ *     the workspace sized by vt_workspace_bytes).  Calls are reentrant and
+ *     thread-safe (no mutable globals); errors are reported per thread.
+ *   - LLRs are int8, stage-major (N, B): element (t, b) at llr[t*B + b], the
+ *     layout of the reference CLI's LLR files (cli.py:136-140).  Positive LLR
+ *     means the coded bit is more likely 0 (reference.py:28).
+ *   - Output bits are packed little-endian: stage t is bit (t & 31) of word
+ *     t >> 5 (np.packbits(..., "little"), cli.py:5-6, 170-171).  `bits` must be
+ *     zero-initialised by the caller: words shared by two windows are OR-ed.
+ *   - Decisions are bit-exact against the reference for integer LLRs: ties
+ *     select the second predecessor (reference.py:121), the final state is the
+ *     lowest-index argmax (reference.py:138).
+ *   - Return 0 on success, a negative VT_E* code on error; vt_last_error()
+ *     returns a message for the calling thread.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ */
+#ifndef VITERTILE_B200_H
+#define VITERTILE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VT_MAX_OUTPUTS 8
+
+/* codes.py:51-107 CodeSpec: constraint length K and B generator polynomials
+ * (bit K-1 taps the current input bit, bit 0 the oldest register bit). */
+typedef struct vt_code {
+  int32_t K;
+  int32_t B;
+  uint32_t gens[VT_MAX_OUTPUTS];
+} vt_code;
+
+enum {
+  VT_OK = 0,
+  VT_EINVAL = -1,      /* bad argument (mirrors the reference's ValueError) */
+  VT_EUNSUPPORTED = -2,/* no compiled kernel for this code */
+  VT_EWORKSPACE = -3,  /* workspace too small */
+  VT_ECUDA = -4        /* CUDA runtime error */
+};
+
+/* Library version (major*10000 + minor*100 + patch). */
+int vt_version(void);
+
+/* 1 if a compiled sm_100a kernel exists for this code, else 0. */
+int vt_code_supported(const vt_code* code);
+
+/* Message describing the last error on the calling thread ("" if none). */
+const char* vt_last_error(void);
+
+/* Workspace (device bytes) needed by vt_decode_stream[_range] / vt_decode_frames
+ * for the given geometry on the current device. */
+size_t vt_workspace_bytes(const vt_code* code, int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1);
+
+/* Decode the whole stream: windows of plan_frames(N, F, V) (framing.py:68-83).
+ * llr: device (N, B) int8; bits: device ceil(N/32) uint32 (zeroed);
+ * final_metric: optional device int64 per window (max path metric). */
+int vt_decode_stream(const vt_code* code, const int8_t* llr, int64_t N, int64_t F, int64_t V, uint32_t* bits,
+                     int64_t* final_metric, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Decode windows [w0, w1) of plan_frames(N, F, V).  llr points at stage st0
+ * of the stream and holds stages [st0, st1); requires st0 % 16 == 0 (or 0),
+ * st0 <= max(0, w0*F - V), st1 >= min(N, min(w1*F, N) + V), llr 16-B aligned.
+ * bits is the packed output of the WHOLE stream (word 0 = stages 0..31);
+ * final_metric (optional) has w1 - w0 entries. */
+int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, int64_t st1, int64_t N, int64_t F,
+                           int64_t V, int64_t w0, int64_t w1, uint32_t* bits, int64_t* final_metric,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* reference.decode_batch: `frames` independent frames of n stages each,
+ * llr device (frames, n, B) int8 (stage-major per frame); bits device packed
+ * output of the concatenation (frame f stage t -> bit f*n + t), zeroed;
+ * final_metric device int64 per frame (nullable). */
+int vt_decode_frames(const vt_code* code, const int8_t* llr, int64_t frames, int64_t n, uint32_t* bits,
+                     int64_t* final_metric, void* workspace, size_t workspace_bytes, void* stream);
+
+/* decode_stream with HOST buffers: llr_host (N, B) int8 -> bits_host
+ * ceil(N/32) words.  Device staging buffers (llr_dev >= N*B bytes rounded up
+ * to 16, bits_dev >= ceil(N/32) words) and the workspace are caller-owned.
+ * The copy is pipelined in `nchunks` window ranges on `stream` (synchronous
+ * on return).  Pinned host memory gives full PCIe bandwidth. */
+int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N, int64_t F, int64_t V,
+                          uint32_t* bits_host, int8_t* llr_dev, uint32_t* bits_dev, void* workspace,
+                          size_t workspace_bytes, int nchunks, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VITERTILE_B200_H */

@@ -1,0 +1,278 @@
+// C ABI of the B200 framed Viterbi decoder (see include/vitertile_b200.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "../../include/vitertile_b200.h"
+#include "vt_common.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(VT_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+constexpr int kNT = 128;  // threads (= windows) per CTA
+
+struct Geometry {
+  int64_t nwin;
+  int nc, b_lo, nbs;
+};
+
+Geometry geometry(int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1) {
+  Geometry g;
+  g.nwin = w1 - w0;
+  const int64_t lmax = std::min<int64_t>(N, F + 2 * V);
+  g.nc = (int)((lmax + 15) / 16);
+  const int64_t head = std::min<int64_t>(N, F + V);  // max (stop - emit_start) over windows
+  int64_t blo = (16 * (int64_t)g.nc - head) / 16;
+  if (blo < 0) blo = 0;
+  g.b_lo = (int)blo;
+  g.nbs = g.nc - g.b_lo;
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// kernel registry: one generated kernel per supported code (gen/registry.inc)
+// ---------------------------------------------------------------------------
+struct KernelEntry {
+  int K, B, T, SL;
+  uint32_t gens[VT_MAX_OUTPUTS];
+  const void* fn;
+};
+
+#define VT_KERNEL(fn_, K_, B_, T_, SL_, ...) {K_, B_, T_, SL_, __VA_ARGS__, (const void*)&fn_},
+#define VT_DECL_ONLY
+}  // namespace
+#include "gen/registry_decl.inc"
+namespace {
+
+const KernelEntry* registry(int* n) {
+  static const KernelEntry table[] = {
+#include "gen/registry.inc"
+  };
+  *n = (int)(sizeof(table) / sizeof(table[0]));
+  return table;
+}
+
+const KernelEntry* find(const vt_code* c) {
+  if (!c) return nullptr;
+  int n;
+  const KernelEntry* t = registry(&n);
+  for (int i = 0; i < n; ++i) {
+    if (t[i].K != c->K || t[i].B != c->B) continue;
+    bool same = true;
+    for (int b = 0; b < c->B; ++b) same = same && t[i].gens[b] == c->gens[b];
+    if (same) return &t[i];
+  }
+  return nullptr;
+}
+
+int validate(const vt_code* c) {
+  if (!c) return fail(VT_EINVAL, "code is NULL");
+  if (c->K < 3 || c->K > 16) return fail(VT_EINVAL, "constraint length %d out of range", c->K);
+  if (c->B < 2 || c->B > VT_MAX_OUTPUTS) return fail(VT_EINVAL, "need 2..%d generators, got %d", VT_MAX_OUTPUTS, c->B);
+  for (int b = 0; b < c->B; ++b)
+    if (c->gens[b] >= (1u << c->K)) return fail(VT_EINVAL, "generator %o does not fit in %d bits", c->gens[b], c->K);
+  return VT_OK;
+}
+
+int device_sms() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+int ctas_per_sm(const KernelEntry* k) {
+  const char* env = getenv("VT_CTAS_PER_SM");
+  if (env && atoi(env) > 0) return atoi(env);
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, kNT, 0) != cudaSuccess || occ < 1) occ = 1;
+  return std::min(occ, 4);
+}
+
+int64_t grid_for(const KernelEntry* k, int64_t nwin) {
+  const int64_t wpc = kNT / k->T;  // windows per CTA
+  const int64_t tiles = (nwin + wpc - 1) / wpc;
+  const int64_t cap = (int64_t)device_sms() * ctas_per_sm(k);
+  return std::max<int64_t>(1, std::min(tiles, cap));
+}
+
+size_t scratch_bytes(const KernelEntry* k, const Geometry& g, int64_t grid) {
+  return (size_t)grid * g.nbs * std::max(k->SL / 8, 1) * kNT * sizeof(uint4);
+}
+
+}  // namespace
+
+extern "C" {
+
+int vt_version(void) { return 100; }
+
+const char* vt_last_error(void) { return g_err; }
+
+int vt_code_supported(const vt_code* code) { return find(code) != nullptr ? 1 : 0; }
+
+size_t vt_workspace_bytes(const vt_code* code, int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1) {
+  const KernelEntry* k = find(code);
+  if (!k || N < 1 || F < 1 || V < 0 || w1 <= w0) return 0;
+  const Geometry g = geometry(N, F, V, w0, w1);
+  return scratch_bytes(k, g, grid_for(k, g.nwin));
+}
+
+int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, int64_t st1, int64_t N, int64_t F,
+                           int64_t V, int64_t w0, int64_t w1, uint32_t* bits, int64_t* final_metric,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  g_err[0] = 0;
+  int rc = validate(code);
+  if (rc) return rc;
+  const KernelEntry* k = find(code);
+  if (!k)
+    return fail(VT_EUNSUPPORTED, "no sm_100a kernel compiled for K=%d B=%d generators (%o, %o, ...)", code->K,
+                code->B, code->gens[0], code->gens[1]);
+  if (N < 1) return fail(VT_EINVAL, "stream must have at least one stage");
+  if (F < 1) return fail(VT_EINVAL, "frame length must be >= 1");
+  if (V < 0) return fail(VT_EINVAL, "overlap must be >= 0");
+  const int64_t nw_total = (N + F - 1) / F;
+  if (w0 < 0 || w1 > nw_total || w0 >= w1) return fail(VT_EINVAL, "window range [%lld, %lld) outside [0, %lld)",
+                                                      (long long)w0, (long long)w1, (long long)nw_total);
+  if (!llr || !bits) return fail(VT_EINVAL, "llr and bits must be device pointers");
+  if (((uintptr_t)llr & 15) != 0) return fail(VT_EINVAL, "llr must be 16-byte aligned");
+  if (st0 != 0 && (st0 % 16) != 0) return fail(VT_EINVAL, "st0 must be a multiple of 16");
+  const int64_t need_lo = std::max<int64_t>(0, w0 * F - V);
+  const int64_t need_hi = std::min<int64_t>(N, std::min<int64_t>(w1 * F, N) + V);
+  if (st0 > need_lo || st1 < need_hi || st1 > N)
+    return fail(VT_EINVAL, "llr stage range [%lld, %lld) does not cover [%lld, %lld)", (long long)st0,
+                (long long)st1, (long long)need_lo, (long long)need_hi);
+
+  const Geometry g = geometry(N, F, V, w0, w1);
+  const int64_t grid = grid_for(k, g.nwin);
+  const size_t need = scratch_bytes(k, g, grid);
+  if (!workspace || workspace_bytes < need)
+    return fail(VT_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+
+  vt::StreamArgs a;
+  a.llr = llr;
+  a.st0 = st0;
+  a.st1 = st1;
+  a.N = N;
+  a.F = F;
+  a.V = V;
+  a.w0 = w0;
+  a.w1 = w1;
+  a.bits = bits;
+  a.final_metric = final_metric;
+  a.scratch = reinterpret_cast<uint4*>(workspace);
+  a.nc = g.nc;
+  a.b_lo = g.b_lo;
+  a.nbs = g.nbs;
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchKernel(k->fn, dim3((unsigned)grid), dim3(kNT), args, 0, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return VT_OK;
+}
+
+int vt_decode_stream(const vt_code* code, const int8_t* llr, int64_t N, int64_t F, int64_t V, uint32_t* bits,
+                     int64_t* final_metric, void* workspace, size_t workspace_bytes, void* stream) {
+  if (F < 1) return fail(VT_EINVAL, "frame length must be >= 1");
+  if (N < 1) return fail(VT_EINVAL, "stream must have at least one stage");
+  return vt_decode_stream_range(code, llr, 0, N, N, F, V, 0, (N + F - 1) / F, bits, final_metric, workspace,
+                                workspace_bytes, stream);
+}
+
+int vt_decode_frames(const vt_code* code, const int8_t* llr, int64_t frames, int64_t n, uint32_t* bits,
+                     int64_t* final_metric, void* workspace, size_t workspace_bytes, void* stream) {
+  if (frames < 1 || n < 1) return fail(VT_EINVAL, "need frames >= 1 and n >= 1");
+  // F independent frames == a stream of frames*n stages cut with F=n, V=0
+  return vt_decode_stream(code, llr, frames * n, n, 0, bits, final_metric, workspace, workspace_bytes, stream);
+}
+
+int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N, int64_t F, int64_t V,
+                          uint32_t* bits_host, int8_t* llr_dev, uint32_t* bits_dev, void* workspace,
+                          size_t workspace_bytes, int nchunks, void* stream) {
+  g_err[0] = 0;
+  int rc = validate(code);
+  if (rc) return rc;
+  if (!find(code)) return fail(VT_EUNSUPPORTED, "no sm_100a kernel compiled for this code");
+  if (N < 1 || F < 1 || V < 0) return fail(VT_EINVAL, "bad geometry");
+  if (!llr_host || !bits_host || !llr_dev || !bits_dev) return fail(VT_EINVAL, "NULL buffer");
+  const int B = code->B;
+  const int64_t nw = (N + F - 1) / F;
+  const int64_t nwords = (N + 31) / 32;
+  if (nchunks < 1) nchunks = 1;
+  if (nchunks > nw) nchunks = (int)nw;
+  cudaStream_t s = (cudaStream_t)stream;
+
+  // copy and compute run on separate streams so chunk i+1's H2D overlaps chunk i's decode
+  static thread_local cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  static thread_local int cs_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cs_dev != dev || !cs_in) {
+    cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking);
+    cs_dev = dev;
+  }
+  cudaError_t e = cudaMemsetAsync(bits_dev, 0, nwords * 4, s);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  cudaEvent_t ev_start;
+  cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+  cudaEventRecord(ev_start, s);
+  cudaStreamWaitEvent(cs_in, ev_start, 0);
+  cudaStreamWaitEvent(cs_out, ev_start, 0);
+
+  int64_t copied_hi = 0, words_done = 0;
+  for (int i = 0; i < nchunks && rc == 0; ++i) {
+    const int64_t w0 = nw * i / nchunks, w1 = nw * (i + 1) / nchunks;
+    const int64_t st0 = (std::max<int64_t>(0, w0 * F - V) / 16) * 16;
+    const int64_t st1 = std::min<int64_t>(N, std::min<int64_t>(w1 * F, N) + V);
+    const int64_t c0 = std::max(st0, copied_hi);
+    if (st1 > c0) {
+      e = cudaMemcpyAsync(llr_dev + c0 * B, llr_host + c0 * B, (size_t)(st1 - c0) * B, cudaMemcpyHostToDevice, cs_in);
+      if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
+      copied_hi = st1;
+    }
+    cudaEvent_t ev_in, ev_k;
+    cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_k, cudaEventDisableTiming);
+    cudaEventRecord(ev_in, cs_in);
+    cudaStreamWaitEvent(s, ev_in, 0);
+    rc = vt_decode_stream_range(code, llr_dev + st0 * B, st0, st1, N, F, V, w0, w1, bits_dev, nullptr, workspace,
+                                workspace_bytes, s);
+    cudaEventRecord(ev_k, s);
+    cudaStreamWaitEvent(cs_out, ev_k, 0);
+    const int64_t wend = (i + 1 == nchunks) ? nwords : std::min<int64_t>(N, w1 * F) / 32;
+    if (rc == 0 && wend > words_done) {
+      e = cudaMemcpyAsync(bits_host + words_done, bits_dev + words_done, (size_t)(wend - words_done) * 4,
+                          cudaMemcpyDeviceToHost, cs_out);
+      if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
+      words_done = wend;
+    }
+    cudaEventDestroy(ev_in);
+    cudaEventDestroy(ev_k);
+  }
+  cudaEvent_t ev_done;
+  cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
+  cudaEventRecord(ev_done, cs_out);
+  cudaStreamWaitEvent(s, ev_done, 0);
+  e = cudaStreamSynchronize(s);
+  cudaEventDestroy(ev_done);
+  cudaEventDestroy(ev_start);
+  if (rc == 0 && e != cudaSuccess) rc = cuda_fail(e, "decode_stream_host");
+  return rc;
+}
+
+}  // extern "C"

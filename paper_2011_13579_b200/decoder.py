@@ -1,0 +1,435 @@
+"""Reference-compatible decode API backed by the sm_100a kernels.
+
+Drop-in for the decode entry points of the reference package
+(pkg/src/vitertile): same names, argument meaning, return types and
+ValueError conventions.  Every decode runs on the GPU through the C ABI of
+include/vitertile_b200.h; there is no CPU fallback.
+
+Parity contract: results are bit-identical to the reference
+for integer-valued LLRs in [-128, 127] (the int8 quantised LLRs the decoder
+is specified on).  Non-integer float LLRs are rejected with ValueError — use
+``quantize_llr`` first; hard mode slices any float input exactly like the
+reference (reference.py:202-203).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import VtCode, check, lib
+from .codes import CodeSpec, find_dragonfly_groups, identical_bomat_classes
+from .framing import FramePlan
+
+__all__ = [
+    "PrecisionPolicy",
+    "TileOpCounter",
+    "DecoderConfig",
+    "MatrixDecodeResult",
+    "SoftFrame",
+    "quantize_llr",
+    "decode_stream",
+    "decode_stream_device",
+    "decode_stream_host",
+    "decode_batch",
+    "decode_reference",
+    "decode_matrix_batch",
+    "decode_matrix",
+    "workspace_bytes",
+]
+
+_PRECISIONS = ("half", "single")
+
+
+@dataclass(frozen=True)
+class PrecisionPolicy:
+    """Accumulator / channel-input precision (tile.py:21-31).  The B200 path
+    accumulates exact int32 metrics; ``accumulator="half"`` (a lossy fp16
+    emulation) is rejected at decode time."""
+
+    accumulator: str = "single"
+    channel_input: str = "single"
+
+    def __post_init__(self) -> None:
+        for name in (self.accumulator, self.channel_input):
+            if name not in _PRECISIONS:
+                raise ValueError(f"unknown precision {name!r}")
+
+
+@dataclass
+class TileOpCounter:
+    """Paper tile-op accounting (tile.py:34-49)."""
+
+    mma_ops: int = 0
+    survivor_write_passes: int = 0
+    stages: int = 0
+
+    @property
+    def ops_per_stage(self) -> float:
+        return self.mma_ops / self.stages if self.stages else 0.0
+
+    def reset(self) -> None:
+        self.mma_ops = self.survivor_write_passes = self.stages = 0
+
+
+@dataclass(frozen=True)
+class DecoderConfig:
+    """Decode path selection (matrix.py:94-105)."""
+
+    radix: int = 2
+    optimized: bool = False
+    policy: PrecisionPolicy = field(default_factory=PrecisionPolicy)
+    renormalize: bool = False
+
+    def __post_init__(self) -> None:
+        if self.radix not in (2, 4):
+            raise ValueError("radix must be 2 or 4")
+
+
+@dataclass
+class MatrixDecodeResult:
+    bits: np.ndarray
+    final_metric: np.ndarray | float
+    counter: TileOpCounter
+
+    @property
+    def q(self) -> float:
+        return self.counter.ops_per_stage
+
+
+@dataclass
+class SoftFrame:
+    """LLR input (B, N); positive LLR favours coded bit 0 (reference.py:27-48)."""
+
+    llr: np.ndarray
+    channel_precision: str = "single"
+
+    def __post_init__(self) -> None:
+        if self.channel_precision not in _PRECISIONS:
+            raise ValueError(f"unknown channel precision {self.channel_precision!r}")
+        arr = np.asarray(self.llr, dtype=np.float64)
+        if arr.ndim != 2 or arr.shape[1] < 1:
+            raise ValueError("LLR input must have shape (B, N) with N >= 1")
+        if not np.all(np.isfinite(arr)):
+            raise ValueError("LLR values must be finite")
+        if self.channel_precision == "half":
+            arr = arr.astype(np.float16).astype(np.float64)
+        self.llr = arr
+
+    @property
+    def num_stages(self) -> int:
+        return self.llr.shape[1]
+
+
+def quantize_llr(llr, scale: float = 16.0) -> np.ndarray:
+    """int8 quantiser the parity contract is defined on:
+    q = clamp(rint(scale * llr), -127, 127)."""
+    return np.clip(np.rint(np.asarray(llr, dtype=np.float64) * scale), -127, 127).astype(np.int8)
+
+
+# ---------------------------------------------------------------------------
+# device plumbing (torch is used only for device memory and streams)
+# ---------------------------------------------------------------------------
+
+_ws_lock = threading.Lock()
+_ws: dict[int, object] = {}
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("vitertile_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    return torch
+
+
+def _workspace(nbytes: int):
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    with _ws_lock:
+        buf = _ws.get(dev)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=f"cuda:{dev}")
+            _ws[dev] = buf
+        return buf
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _code(spec: CodeSpec) -> VtCode:
+    c = VtCode.from_spec(spec)
+    if not lib().vt_code_supported(ctypes.byref(c)):
+        raise NotImplementedError(
+            f"no sm_100a kernel was generated for K={spec.constraint_length} generators "
+            f"{spec.octal_generators}; add it to csrc/gen_kernels.py STANDARD_CODES and rebuild")
+    return c
+
+
+def workspace_bytes(spec: CodeSpec, n: int, frame_len: int, overlap: int, w0: int = 0, w1: int | None = None) -> int:
+    nw = -(-int(n) // int(frame_len))
+    w1 = nw if w1 is None else w1
+    return int(lib().vt_workspace_bytes(ctypes.byref(_code(spec)), int(n), int(frame_len), int(overlap), int(w0),
+                                        int(w1)))
+
+
+def _as_int8_llr(llr, what: str = "LLR") -> np.ndarray:
+    a = np.asarray(llr)
+    if a.dtype == np.int8:
+        return a
+    if np.issubdtype(a.dtype, np.integer):
+        if a.size and (a.min() < -128 or a.max() > 127):
+            raise ValueError(f"{what} values must lie in [-128, 127] (int8 quantised LLRs)")
+        return a.astype(np.int8)
+    af = np.asarray(a, dtype=np.float64)
+    if not np.all(np.isfinite(af)):
+        raise ValueError("LLR values must be finite")
+    q = np.rint(af)
+    if not np.array_equal(q, af):
+        raise ValueError(f"{what} must be integer-valued int8 quantised LLRs; quantise with quantize_llr() "
+                         "(the B200 decoder is bit-exact on the quantised integers)")
+    if q.size and (q.min() < -128 or q.max() > 127):
+        raise ValueError(f"{what} values must lie in [-128, 127] (int8 quantised LLRs)")
+    return q.astype(np.int8)
+
+
+def _unpack(words_np: np.ndarray, n: int) -> np.ndarray:
+    return np.unpackbits(words_np.view(np.uint8), count=n, bitorder="little")
+
+
+# ---------------------------------------------------------------------------
+# device-level entry points (no host round trip)
+# ---------------------------------------------------------------------------
+
+
+def decode_stream_device(llr_nb, spec: CodeSpec, frame_len: int, overlap: int, *, out=None,
+                         final_metric=None, stream=None):
+    """Decode an int8 (N, B) device tensor with plan_frames(N, F, V) windows.
+
+    Returns the packed output bits as an int32 device tensor of ceil(N/32)
+    words (bit t&31 of word t>>5 = decoded bit of stage t).  ``out`` may be a
+    zeroed int32 tensor to reuse; ``final_metric`` an int64 device tensor with
+    one entry per window."""
+    torch = _torch()
+    code = _code(spec)
+    if llr_nb.dtype != torch.int8 or llr_nb.dim() != 2 or llr_nb.shape[1] != spec.outputs_per_bit:
+        raise ValueError("llr must be an int8 (N, B) CUDA tensor")
+    llr_nb = llr_nb.contiguous()
+    n = int(llr_nb.shape[0])
+    nwords = (n + 31) // 32
+    if out is None:
+        out = torch.zeros(nwords, dtype=torch.int32, device=llr_nb.device)
+    nw = -(-n // int(frame_len))
+    need = lib().vt_workspace_bytes(ctypes.byref(code), n, int(frame_len), int(overlap), 0, nw)
+    ws = _workspace(need)
+    check(lib().vt_decode_stream(ctypes.byref(code), _ptr(llr_nb), n, int(frame_len), int(overlap), _ptr(out),
+                                 _ptr(final_metric), _ptr(ws), ws.numel(), _stream_ptr(stream)))
+    return out
+
+
+def decode_stream_host(llr_nb_host, spec: CodeSpec, frame_len: int, overlap: int, *, bits_host=None,
+                       nchunks: int = 8, stream=None):
+    """End-to-end decode through the C-ABI host entry (vt_decode_stream_host):
+    int8 (N, B) host tensor (pinned for full PCIe bandwidth) -> packed int32
+    host tensor.  H2D, decode and D2H are pipelined in ``nchunks`` window ranges."""
+    torch = _torch()
+    code = _code(spec)
+    n = int(llr_nb_host.shape[0])
+    b = spec.outputs_per_bit
+    nwords = (n + 31) // 32
+    if bits_host is None:
+        bits_host = torch.empty(nwords, dtype=torch.int32, pin_memory=True)
+    dev = torch.cuda.current_device()
+    key = ("host", dev)
+    with _ws_lock:
+        stg = _ws.get(key)
+        need_llr = ((n * b + 15) // 16) * 16
+        if stg is None or stg[0].numel() < need_llr or stg[1].numel() < nwords:
+            stg = (torch.empty(need_llr, dtype=torch.int8, device=f"cuda:{dev}"),
+                   torch.empty(nwords, dtype=torch.int32, device=f"cuda:{dev}"))
+            _ws[key] = stg
+    nw = -(-n // int(frame_len))
+    need = 0
+    for i in range(max(1, min(nchunks, nw))):
+        w0, w1 = nw * i // nchunks, nw * (i + 1) // nchunks
+        if w1 > w0:
+            need = max(need, lib().vt_workspace_bytes(ctypes.byref(code), n, int(frame_len), int(overlap), w0, w1))
+    ws = _workspace(need)
+    check(lib().vt_decode_stream_host(ctypes.byref(code), _ptr(llr_nb_host), n, int(frame_len), int(overlap),
+                                      _ptr(bits_host), _ptr(stg[0]), _ptr(stg[1]), _ptr(ws), ws.numel(),
+                                      int(nchunks), _stream_ptr(stream)))
+    return bits_host
+
+
+def _decode_frames_np(frames_fnb: np.ndarray, spec: CodeSpec):
+    """(F, N, B) int8 frames -> (bits (F, N) uint8, final metric int64 (F,))."""
+    torch = _torch()
+    code = _code(spec)
+    f, n, _ = frames_fnb.shape
+    dev_llr = torch.from_numpy(np.ascontiguousarray(frames_fnb)).cuda()
+    total = f * n
+    bits = torch.zeros((total + 31) // 32, dtype=torch.int32, device=dev_llr.device)
+    metric = torch.empty(f, dtype=torch.int64, device=dev_llr.device)
+    need = lib().vt_workspace_bytes(ctypes.byref(code), total, n, 0, 0, f)
+    ws = _workspace(need)
+    check(lib().vt_decode_frames(ctypes.byref(code), _ptr(dev_llr), f, n, _ptr(bits), _ptr(metric), _ptr(ws),
+                                 ws.numel(), _stream_ptr(None)))
+    words = bits.cpu().numpy()
+    return _unpack(words, total).reshape(f, n), metric.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible API
+# ---------------------------------------------------------------------------
+
+
+def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "reference",
+                  config: DecoderConfig | None = None, workers: int = 1) -> np.ndarray:
+    """framing.decode_stream (framing.py:96-141): decode a (B, N) LLR stream
+    window by window and stitch the emit ranges -> uint8 bits (N,).
+    ``workers`` is accepted for signature compatibility (the GPU decodes all
+    windows of the plan in one launch)."""
+    arr = np.asarray(llr)
+    if arr.ndim != 2 or arr.shape[1] != plan.total_stages:
+        raise ValueError("plan does not match stream length")
+    if decoder not in ("reference", "matrix"):
+        raise ValueError(f"unknown decoder {decoder!r}")
+    if arr.shape[0] != spec.outputs_per_bit:
+        raise ValueError("LLR input must have shape (B, N)")
+    if decoder == "matrix":
+        _check_matrix_config(spec, config or DecoderConfig())
+    q = _as_int8_llr(arr).T.copy()  # (N, B) stage-major
+    torch = _torch()
+    n = q.shape[0]
+    pinned = torch.from_numpy(q).pin_memory()
+    words = decode_stream_host(pinned, spec, plan.frame_len, plan.overlap)
+    return _unpack(words.numpy(), n)
+
+
+def decode_batch(llrs, spec: CodeSpec, mode: str = "soft", renormalize: bool = False):
+    """reference.decode_batch (reference.py:194-206): frames (F, B, N) ->
+    (bits (F, N) uint8, final metric per frame float64)."""
+    arr = np.asarray(llrs, dtype=np.float64)
+    if arr.ndim != 3 or arr.shape[1] != spec.outputs_per_bit:
+        raise ValueError("LLR batch must have shape (F, B, N)")
+    if mode == "hard":
+        arr = np.where(arr >= 0.0, 1.0, -1.0)
+    elif mode != "soft":
+        raise ValueError(f"unknown mode {mode!r}")
+    q = _as_int8_llr(arr)
+    bits, metric = _decode_frames_np(np.transpose(q, (0, 2, 1)), spec)
+    if renormalize:  # reference.py:124-125: max subtracted after every stage -> final max is 0
+        metric = np.zeros_like(metric)
+    return bits, metric.astype(np.float64)
+
+
+def _to_soft(frame, spec: CodeSpec, mode: str) -> np.ndarray:
+    # reference.py:167-178
+    llr = frame.llr if isinstance(frame, SoftFrame) else np.asarray(frame, dtype=np.float64)
+    if llr.ndim != 2 or llr.shape[0] != spec.outputs_per_bit:
+        raise ValueError("LLR input must have shape (B, N)")
+    if mode == "hard":
+        if not np.all((llr == 0) | (llr == 1)):
+            raise ValueError("hard mode expects a bit array")
+        llr = 1.0 - 2.0 * llr
+    elif mode != "soft":
+        raise ValueError(f"unknown mode {mode!r}")
+    return llr
+
+
+def decode_reference(frame, spec: CodeSpec, mode: str = "soft", initial_metrics=None,
+                     renormalize: bool = False) -> np.ndarray:
+    """reference.decode_reference (reference.py:181-191): one frame, forward +
+    traceback -> bits (N,)."""
+    llr = _to_soft(frame, spec, mode)
+    if initial_metrics is not None:
+        init = np.broadcast_to(np.asarray(initial_metrics, dtype=np.float64), (spec.num_states,))
+        if not np.all(init == init[0]):
+            raise NotImplementedError("non-uniform initial metrics are not supported by the B200 kernels "
+                                      "(each window starts from all-zero metrics, SPEC.md:216)")
+    bits, _ = decode_batch(llr[None, :, :], spec, renormalize=renormalize)
+    return bits[0]
+
+
+# ---------------------------------------------------------------------------
+# tile-decoder API (matrix.py:342-422)
+# ---------------------------------------------------------------------------
+
+_BLOCK, _TILE_BLOCKS = 4, 4  # 4 columns per block, 4 blocks per 16x16 tile
+
+
+def _tiles(blocks: int) -> int:
+    return -(-blocks // _TILE_BLOCKS)
+
+
+def _radix2_tiles(spec: CodeSpec) -> int:
+    if spec.outputs_per_bit > _BLOCK:
+        raise ValueError(f"butterfly output matrix width {spec.outputs_per_bit} exceeds block width {_BLOCK}")
+    return _tiles(sum(-(-len(c) // _BLOCK) for c in identical_bomat_classes(1, spec)))
+
+
+def _radix4_tiles(spec: CodeSpec, optimized: bool) -> tuple[int, bool]:
+    if 2 * spec.outputs_per_bit > _BLOCK:
+        raise ValueError(f"super-branch output width {2 * spec.outputs_per_bit} exceeds block width {_BLOCK}")
+    plain = sum(-(-len(c) // _BLOCK) for c in identical_bomat_classes(2, spec))
+    if optimized:
+        grouped = sum(-(-len(g.members) // _BLOCK) for g in find_dragonfly_groups(2, spec))
+        if grouped < plain:
+            return _tiles(grouped), True
+    return _tiles(plain), False
+
+
+def _check_matrix_config(spec: CodeSpec, config: DecoderConfig) -> tuple[int, int, bool]:
+    if config.policy.accumulator == "half":
+        raise NotImplementedError("accumulator='half' is a lossy fp16 emulation; the B200 decoder accumulates "
+                                  "exact integer metrics and does not reproduce it")
+    t2 = _radix2_tiles(spec)
+    t4, effective = (_radix4_tiles(spec, config.optimized) if config.radix == 4 else (0, False))
+    if config.radix == 4 and config.optimized and effective:
+        raise NotImplementedError("radix-4 with the dragonfly-group permutation (optimized=True) breaks ties in "
+                                  "permuted order (matrix.py:329-333); that tie order is not yet implemented "
+                                  "on sm_100a (use optimized=False, which is bit-identical to the reference)")
+    return t2, t4, effective
+
+
+def decode_matrix_batch(llrs, spec: CodeSpec, config: DecoderConfig | None = None) -> MatrixDecodeResult:
+    """matrix.decode_matrix_batch (matrix.py:342-386) on the B200 kernels.
+
+    Radix-2 and radix-4 (non-optimised) decisions equal two-stage radix-2 ACS
+    with the natural tie rule, so the same exact
+    kernel serves both; the counter reports the paper's tile-op accounting."""
+    config = config or DecoderConfig()
+    arr = np.asarray(llrs, dtype=np.float32)
+    if arr.ndim != 3 or arr.shape[1] != spec.outputs_per_bit:
+        raise ValueError("LLR batch must have shape (F, B, N)")
+    f, _, n = arr.shape
+    t2, t4, _ = _check_matrix_config(spec, config)
+    # matrix.py:290,320 (and 354-355): LLRs pass through binary16; exact for int8 values
+    arr = arr.astype(np.float16).astype(np.float64)
+    q = _as_int8_llr(arr)
+    bits, metric = _decode_frames_np(np.transpose(q, (0, 2, 1)), spec)
+    counter = TileOpCounter()
+    if config.radix == 2:
+        counter.mma_ops = t2 * n
+        counter.survivor_write_passes = n
+    else:
+        counter.mma_ops = t4 * (n // 2) + t2 * (n % 2)
+        counter.survivor_write_passes = n // 2 + n % 2
+    counter.stages = n
+    return MatrixDecodeResult(bits=bits, final_metric=metric.astype(np.float64), counter=counter)
+
+
+def decode_matrix(frame, spec: CodeSpec, config: DecoderConfig | None = None) -> MatrixDecodeResult:
+    """matrix.decode_matrix (matrix.py:412-422): single-frame wrapper."""
+    llr = getattr(frame, "llr", frame)
+    res = decode_matrix_batch(np.asarray(llr)[None, :, :], spec, config)
+    return MatrixDecodeResult(bits=res.bits[0], final_metric=float(res.final_metric[0]), counter=res.counter)

@@ -1,0 +1,146 @@
+"""GPU parity: sm_100a decoder vs the reference (golden vectors) and vs the
+C oracle on larger seeded inputs.  Bit-exact equality is required."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN, code_params, cuda_available, golden_cases
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+STREAM, CODES = golden_cases("stream")
+BATCH, _ = golden_cases("batch")
+MATRIX, _ = golden_cases("matrix")
+
+
+@pytest.fixture(scope="module")
+def z():
+    return np.load(GOLDEN)
+
+
+@pytest.fixture(scope="module")
+def vt():
+    import paper_2011_13579_b200 as vt
+    return vt
+
+
+def _spec(vt, name):
+    k, gens = code_params(CODES, name)
+    return vt.CodeSpec(k, gens)
+
+
+def _device_decode(vt, llr_nb, spec, f, v):
+    import torch
+    words = vt.decode_stream_device(torch.from_numpy(np.ascontiguousarray(llr_nb)).cuda(), spec, f, v)
+    torch.cuda.synchronize()
+    return np.unpackbits(words.cpu().numpy().view(np.uint8), count=llr_nb.shape[0], bitorder="little")
+
+
+@pytest.mark.parametrize("case", STREAM, ids=[f"{c['code']}-{c['tag']}" for c in STREAM])
+def test_stream_matches_reference_golden(vt, z, case):
+    spec = _spec(vt, case["code"])
+    llr = z[case["key"] + "_llr"]
+    want = np.unpackbits(z[case["key"] + "_bits"], count=case["n"], bitorder="little")
+    got = _device_decode(vt, llr, spec, case["frame_len"], case["overlap"])
+    np.testing.assert_array_equal(got, want)
+    # the reference-facing API (host (B, N) array in, uint8 bits out)
+    plan = vt.plan_frames(case["n"], case["frame_len"], case["overlap"])
+    np.testing.assert_array_equal(vt.decode_stream(llr.T.astype(np.float64), spec, plan), want)
+
+
+@pytest.mark.parametrize("case", BATCH, ids=[f"{c['code']}-n{c['n']}-{c['mode']}-r{int(c['renormalize'])}"
+                                              for c in BATCH])
+def test_batch_matches_reference_golden(vt, z, case):
+    spec = _spec(vt, case["code"])
+    bits, metric = vt.decode_batch(z[case["key"] + "_llr"].astype(np.float64), spec, mode=case["mode"],
+                                   renormalize=case["renormalize"])
+    np.testing.assert_array_equal(bits, z[case["key"] + "_bits"])
+    np.testing.assert_array_equal(metric, z[case["key"] + "_metric"])
+
+
+@pytest.mark.parametrize("case", MATRIX, ids=[f"{c['code']}-n{c['n']}-r{c['radix']}{'o' if c['optimized'] else ''}"
+                                               f"-{int(c['renormalize'])}" for c in MATRIX])
+def test_matrix_matches_reference_golden(vt, z, case):
+    spec = _spec(vt, case["code"])
+    cfg = vt.DecoderConfig(radix=case["radix"], optimized=case["optimized"], renormalize=case["renormalize"])
+    llr = z[case["key"] + "_llr"].astype(np.float64)
+    if case["radix"] == 4 and case["optimized"] and case["code"] == "k7r2":
+        with pytest.raises(NotImplementedError):
+            vt.decode_matrix_batch(llr, spec, cfg)
+        return
+    res = vt.decode_matrix_batch(llr, spec, cfg)
+    np.testing.assert_array_equal(res.bits, z[case["key"] + "_bits"])
+    np.testing.assert_array_equal(res.final_metric, z[case["key"] + "_metric"])
+    c = z[case["key"] + "_counter"]
+    assert (res.counter.mma_ops, res.counter.survivor_write_passes, res.counter.stages) == tuple(int(x) for x in c)
+
+
+@pytest.mark.parametrize("code", ["k7r2", "k7r3", "k9r2", "k8r2", "k5r2"])
+@pytest.mark.parametrize("fv", [(256, 42), (64, 20), (1000, 100), (37, 5), (256, 0)])
+def test_random_streams_match_oracle(vt, code, fv):
+    k, gens = code_params(CODES, code)
+    spec = vt.CodeSpec(k, gens)
+    f, v = fv
+    n = 60_000 if k <= 7 else 20_000
+    _, q = oracle.synthetic_stream(n, k, gens, ebn0_db=1.5, seed=hash((code, fv)) & 0xFFFF, scale=20.0)
+    want = oracle.decode_stream(q, k, gens, f, v, threads=8)
+    np.testing.assert_array_equal(_device_decode(vt, q, spec, f, v), want)
+
+
+def test_tie_heavy_and_extreme_llrs_match_oracle(vt):
+    spec = vt.default_spec()
+    rng = np.random.default_rng(5)
+    for q in (rng.integers(-1, 2, size=(30_000, 2)).astype(np.int8),
+              rng.choice(np.array([-128, 127], dtype=np.int8), size=(30_000, 2)),
+              np.full((5000, 2), -128, dtype=np.int8)):
+        want = oracle.decode_stream(q, 7, (0o171, 0o133), 256, 42, threads=8)
+        np.testing.assert_array_equal(_device_decode(vt, q, spec, 256, 42), want)
+
+
+def test_window_ranges_on_sub_buffers_match_whole(vt):
+    """vt_decode_stream_range on stage sub-buffers (the multi-GPU shard path)."""
+    import ctypes
+    import torch
+    from paper_2011_13579_b200 import _lib
+    from paper_2011_13579_b200.decoder import _code, _ptr, _workspace
+    spec = vt.default_spec()
+    n, f, v = 100_000, 256, 42
+    _, q = oracle.synthetic_stream(n, 7, (0o171, 0o133), ebn0_db=2.0, seed=17)
+    whole = _device_decode(vt, q, spec, f, v)
+    nw = -(-n // f)
+    dev = torch.from_numpy(q).cuda()
+    out = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    code = _code(spec)
+    for w0, w1 in ((0, 100), (100, 101), (101, 250), (250, nw)):
+        st0 = (max(0, w0 * f - v) // 16) * 16
+        st1 = min(n, min(w1 * f, n) + v)
+        sub = dev[st0:st1].clone()  # separate 16B-aligned allocation holding only the shard's stages
+        need = _lib.lib().vt_workspace_bytes(ctypes.byref(code), n, f, v, w0, w1)
+        ws = _workspace(need)
+        _lib.check(_lib.lib().vt_decode_stream_range(ctypes.byref(code), _ptr(sub), st0, st1, n, f, v, w0, w1,
+                                                     _ptr(out), None, _ptr(ws), ws.numel(), None))
+    torch.cuda.synchronize()
+    got = np.unpackbits(out.cpu().numpy().view(np.uint8), count=n, bitorder="little")
+    np.testing.assert_array_equal(got, whole)
+
+
+def test_host_entry_matches_device_entry(vt):
+    import torch
+    spec = vt.default_spec()
+    n = 200_003
+    _, q = oracle.synthetic_stream(n, 7, (0o171, 0o133), ebn0_db=2.5, seed=23)
+    want = _device_decode(vt, q, spec, 256, 42)
+    for chunks in (1, 3, 16):
+        words = vt.decode_stream_host(torch.from_numpy(q).pin_memory(), spec, 256, 42, nchunks=chunks)
+        got = np.unpackbits(words.numpy().view(np.uint8), count=n, bitorder="little")
+        np.testing.assert_array_equal(got, want)
+
+
+def test_final_metrics_match_oracle(vt):
+    spec = vt.CodeSpec(7, (0o133, 0o171, 0o165))
+    rng = np.random.default_rng(9)
+    llrs = rng.integers(-128, 128, size=(300, 3, 500)).astype(np.int8)
+    want_bits, want_metric = oracle.decode_batch(llrs, 7, (0o133, 0o171, 0o165))
+    bits, metric = vt.decode_batch(llrs.astype(np.float64), spec)
+    np.testing.assert_array_equal(bits, want_bits)
+    np.testing.assert_array_equal(metric, want_metric.astype(np.float64))
