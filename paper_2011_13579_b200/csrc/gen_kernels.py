@@ -1,30 +1,37 @@
 #!/usr/bin/env python3
 """Generate straight-line sm_100a ACS kernels, one per convolutional code.
 
-Why a generator: the add-compare-select recursion for 2^(K-1) states over a
-16-stage block is ~2,100 independent integer ops per thread.  Written as C++
-loops over register arrays, NVVM needs minutes per kernel and spends ~2x the
-registers; emitted as straight-line SSA code it compiles in about a second and
-ptxas sees exactly the dataflow we want (IMAD.IADD on the FMA pipe feeding one
-DPX VIADDMNMX on the ALU pipe per state-stage).
+Why a generator: the add-compare-select recursion for 2^(K-1) states is ~130
+independent integer ops per thread per stage.  Written as C++ loops over
+register arrays, NVVM needs minutes per kernel and ~2x the registers; emitted
+as straight-line SSA code it compiles in about a second and ptxas sees exactly
+the intended dataflow: IMAD.IADD on the FMA pipe feeding one DPX VIADDMNMX on
+the ALU pipe per state-stage.
 
 Reference semantics implemented (pkg/src/vitertile):
   * reference.py:60-83  predecessors i0 = 2*(j mod 2^(K-2)), i1 = i0+1, input u = j >> (K-2)
   * codes.py:183-193    branch output bit b = parity(g_b & ((u << (K-1)) | i))
   * reference.py:86-92,119-120  branch metric = sum_b (1 - 2*bit_b) * llr_b (maximised)
   * reference.py:121    tie -> second predecessor: the i1 candidate carries +2^p in the
-                        history bits, so signed max picks it on equal metrics
+                        low history bits, so signed max picks it on equal metrics
   * reference.py:124-125 renormalisation (exact): -lambda_0 folded into the branch metrics
   * reference.py:138    final state = lowest-index argmax
   * framing.py:68-141   windows / emit ranges (vt_common.cuh)
 
+Loop structure.  The inner body is P = K-1 stages: after K-1 radix-2 stages
+the state->register naming returns to the identity, so the loop back-edge
+needs no register moves, and the body (~6 stages of code for K=7) stays small
+enough for the instruction cache.  A history block is NIT = floor(16/P)
+bodies (BL = P*NIT <= 16 stages, 12 for K=7): each state's low 16 bits record
+the survivor-path decisions of the block and are streamed out at block end.
+
 Threads per window T: K <= 7 keeps all 2^(K-1) metrics in one thread (T=1).
-K = 8, 9 spread them over T = 2, 4 lanes.  With the lanes partitioned by tau =
-log2(T) state bits that start at the top, a radix-2 stage maps a partition at
-bits [lo, lo+tau) onto [lo-1, lo-1+tau) with no data exchange, so K-1-tau stages
-run exchange-free; then one shared-memory transpose restores the top-bit
-partition.  The lane-dependent part of the branch parity is a per-lane LLR sign
-flip, so all lanes execute identical code.
+K = 8, 9 spread them over T = 2, 4 lanes.  Lanes are partitioned by tau =
+log2(T) state bits starting at the top; a radix-2 stage maps a partition at
+bits [lo, lo+tau) onto [lo-1, lo-1+tau) with no exchange, so P = K-1-tau
+stages run exchange-free and one shared-memory transpose restores the top-bit
+partition at the end of each body.  The lane-dependent part of the branch
+parity is a per-lane LLR sign flip, so all lanes execute identical code.
 """
 from __future__ import annotations
 
@@ -32,7 +39,7 @@ import argparse
 import os
 
 STANDARD_CODES = {
-    # name: (K, generators as octal strings)   -- BASELINE.json configs + tests/conftest.py:7-15
+    # name: (K, generators as octal strings) -- BASELINE.json configs + tests/conftest.py:7-15
     "k7r2": (7, ("171", "133")),
     "k7r3": (7, ("133", "171", "165")),
     "k9r2": (9, ("753", "561")),
@@ -67,8 +74,13 @@ class Gen:
         self.tau = T.bit_length() - 1
         assert 1 << self.tau == T
         self.SL = self.S // T
-        assert self.SL % 8 == 0 or self.SL < 8, "slots per lane must pack into uint4 groups"
-        self.period = (self.k - self.tau) if T > 1 else 10 ** 9
+        self.SQ = max(self.SL // 8, 1)  # uint4 groups of histories per lane per block
+        self.P = self.k - self.tau  # stages per loop body
+        self.NIT = 16 // self.P
+        self.BL = self.P * self.NIT  # history block length (stages)
+        self.NL = self.B + 1  # staged 16-byte LLR words per block
+        self.NWC = -(-self.BL * self.B // 4)  # realigned LLR words per block
+        assert self.NWC + 4 <= 4 * self.NL
         self.lines: list[str] = []
 
     # -- state <-> (lane, slot) maps for a partition at bits [lo, lo+tau) --------
@@ -89,30 +101,22 @@ class Gen:
     def emit(self, s: str = ""):
         self.lines.append(s)
 
-    # -- one 16-stage block ----------------------------------------------------
-    def block(self, cur: list[str], lo: int) -> tuple[list[str], int, list[int]]:
-        """Emit 16 stages starting from names `cur` in partition `lo`.
-        Returns (names, partition at block end, exchange positions)."""
-        B = self.B
-        n_in_group = 0
-        xchg = []
-        for q in range(16):
-            if self.T > 1 and n_in_group == self.period:
-                cur = self.exchange(cur, lo, tag=f"q{q}")
-                lo = self.k - self.tau
-                n_in_group = 0
-                xchg.append(q)
+    # -- loop body: P stages (+ exchange back to the top partition when T > 1) --
+    def body(self, ind: str) -> None:
+        B, P = self.B, self.P
+        top = self.k - self.tau if self.tau else 0
+        cur = [f"m{r}" for r in range(self.SL)]
+        lo = top
+        for q in range(P):
             lo_out = lo - 1 if self.tau else lo
-            # LLRs of this stage (bytes q*B + b of the chunk), as llr << 16
             for b in range(B):
                 byte = q * B + b
                 expr = f"vt::llr_hi16(cur[{byte >> 2}], {byte & 3}u)"
                 if self.T > 1:
-                    expr = f"{expr} * f{n_in_group}_{b}"
-                self.emit(f"      const int32_t L{q}_{b} = {expr};")
+                    expr = f"{expr} * f{q}_{b}"
+                self.emit(f"{ind}const int32_t L{q}_{b} = {expr};")
+            body, need_d, need_e = [], set(), set()
             outs = []
-            body = []
-            need_d, need_e = set(), set()
             for r in range(self.SL):
                 j = self.state_of(r, 0, lo_out)
                 u = j >> (self.k - 1)
@@ -125,165 +129,201 @@ class Gen:
                 need_d.add(p0)
                 need_e.add(p1)
                 nm = f"x{q}_{r}"
-                body.append(f"      const int32_t {nm} = vt::addmax({cur[r0]}, D{q}_{p0}, "
+                body.append(f"{ind}const int32_t {nm} = vt::addmax({cur[r0]}, D{q}_{p0}, "
                             f"vt::add_fma({cur[r1]}, E{q}_{p1}));")
                 outs.append(nm)
             for p in sorted(need_d | need_e):
-                terms = []
-                for b in range(B):
-                    sgn = "-" if (p >> b) & 1 else "+"
-                    terms.append(f"{sgn} L{q}_{b}")
+                terms = [f"{'-' if (p >> b) & 1 else '+'} L{q}_{b}" for b in range(B)]
                 expr = " ".join(terms).lstrip("+ ")
                 if q == 0:
                     expr = f"{expr} - rfold"
-                self.emit(f"      const int32_t D{q}_{p} = {expr};")
-                if p in need_e:
-                    self.emit(f"      const int32_t E{q}_{p} = D{q}_{p} + {1 << q};")
+                self.emit(f"{ind}const int32_t D{q}_{p} = {expr};")
+                if p in need_e:  # history code 2^(q + P*it) = (1 << q) * cmul, on the FMA pipe
+                    self.emit(f"{ind}const int32_t E{q}_{p} = vt::mad_fma(cmul, {1 << q}, D{q}_{p});")
             self.lines.extend(body)
-            cur = outs
-            lo = lo_out
-            n_in_group += 1
-        return cur, lo, xchg
+            cur, lo = outs, lo_out
+        if self.T > 1:
+            cur = self.exchange(cur, lo, ind)
+        for r in range(self.SL):
+            self.emit(f"{ind}m{r} = {cur[r]};")
 
-    def exchange(self, cur: list[str], lo: int, tag: str) -> list[str]:
+    def exchange(self, cur: list[str], lo: int, ind: str) -> list[str]:
         """Shared-memory transpose from partition `lo` to the top-bit partition."""
         top = self.k - self.tau
-        self.emit(f"      // exchange ({tag}): partition [{lo},{lo + self.tau}) -> [{top},{top + self.tau})")
-        self.emit("      __syncwarp();")
+        self.emit(f"{ind}// exchange: partition [{lo},{lo + self.tau}) -> [{top},{top + self.tau})")
+        self.emit(f"{ind}__syncwarp();")
         r = 0
         while r < self.SL:
             s0 = self.state_of(r, 0, lo)
             run = 1
-            while (r + run < self.SL and self.state_of(r + run, 0, lo) == s0 + run and run < 4):
+            while r + run < self.SL and self.state_of(r + run, 0, lo) == s0 + run and run < 4:
                 run += 1
             if run == 4 and s0 % 4 == 0:
-                self.emit(f"      *reinterpret_cast<int4*>(xw + {s0} + (t << {lo})) = "
+                self.emit(f"{ind}*reinterpret_cast<int4*>(xw + {s0} + (t << {lo})) = "
                           f"make_int4({cur[r]}, {cur[r + 1]}, {cur[r + 2]}, {cur[r + 3]});")
                 r += 4
             else:
-                self.emit(f"      xw[{s0} + (t << {lo})] = {cur[r]};")
+                self.emit(f"{ind}xw[{s0} + (t << {lo})] = {cur[r]};")
                 r += 1
-        self.emit("      __syncwarp();")
+        self.emit(f"{ind}__syncwarp();")
         out = []
         for r in range(0, self.SL, 4):
-            nm = f"y{tag}_{r}"
-            self.emit(f"      const int4 {nm} = *reinterpret_cast<const int4*>(xr + {r});")
+            nm = f"yx_{r}"
+            self.emit(f"{ind}const int4 {nm} = *reinterpret_cast<const int4*>(xr + {r});")
             out += [f"{nm}.x", f"{nm}.y", f"{nm}.z", f"{nm}.w"]
         return out
+
+    def shift_cur(self, ind: str) -> None:
+        """cur <- cur advanced by P*B bytes (the next body's stages)."""
+        nb = self.P * self.B
+        qw, rb = nb // 4, nb % 4
+        for i in range(self.NWC):
+            a = f"cur[{i + qw}]" if i + qw < self.NWC else "0u"
+            if rb == 0:
+                self.emit(f"{ind}cur[{i}] = {a};")
+            else:
+                b = f"cur[{i + qw + 1}]" if i + qw + 1 < self.NWC else "0u"
+                self.emit(f"{ind}cur[{i}] = __funnelshift_r({a}, {b}, {8 * rb});")
 
     # -- whole kernel ----------------------------------------------------------
     def kernel(self) -> str:
         K, B, S, SL, T, tau = self.K, self.B, self.S, self.SL, self.T, self.tau
+        BL, NL, NWC, SQ, P, NIT = self.BL, self.NL, self.NWC, self.SQ, self.P, self.NIT
         WPC = NT // T
-        xstride = S + (4 if T > 1 else 0)
+        xstride = S + 4
+        top = self.k - tau if tau else 0
         name = f"vtk_{self.name}"
         e = self.emit
         e("// GENERATED by gen_kernels.py -- do not edit.")
-        e(f"// code {self.name}: K={K}, generators (octal) {', '.join(oct(g)[2:] for g in self.gens)}, "
-          f"{T} lane(s) per window, {SL} metrics per lane")
+        e(f"// code {self.name}: K={K}, generators (octal) {', '.join(oct(g)[2:] for g in self.gens)}; "
+          f"{T} lane(s)/window, {SL} metrics/lane, {P}-stage body x {NIT} = {BL}-stage history blocks")
         e('#include "../vt_common.cuh"')
         e("")
         e(f'extern "C" __global__ void __launch_bounds__({NT}, 1) {name}(const vt::StreamArgs a) {{')
-        e(f"  constexpr int B = {B};")
+        e(f"  constexpr int B = {B}, K = {K}, BL = {BL}, NL = {NL}, NWC = {NWC};")
         e("  const int tid = threadIdx.x;")
         e(f"  const int t = tid & {T - 1};")
         e(f"  const int wloc = tid >> {tau};")
+        e(f"  __shared__ __align__(16) uint4 s_llr[NL * {NT}];")
+        e(f"  __shared__ uint32_t s_tb[{NT}];")
         if T > 1:
             e(f"  __shared__ __align__(16) int32_t xs[{WPC} * {xstride}];")
             e(f"  int32_t* const xw = xs + wloc * {xstride};")
-            e(f"  const int32_t* const xr = xw + (t << {self.k - tau});")
-            e("  const unsigned gmask = 0xFFFFFFFFu;")
-            e(f"  const int lane0 = (tid & 31) & ~{T - 1};")
-            # per-lane LLR sign flips for stage n of an exchange period
-            for n in range(min(self.period, 16)):
-                lo_in = self.k - tau - n
+            e(f"  const int32_t* const xr = xw + (t << {top});")
+            e("  const int lane0 = (tid & 31) & ~%d;" % (T - 1))
+            for n in range(P):
+                lo_in = top - n
                 for b, g in enumerate(self.gens):
                     e(f"  const int32_t f{n}_{b} = 1 - 2 * (__popc({g}u & ((unsigned)t << {lo_in})) & 1);")
+        e("  const uint64_t pol_first = vt::policy_evict_first();")
+        e("  const uint64_t pol_last = vt::policy_evict_last();")
         e("  const int64_t nwin = a.w1 - a.w0;")
         e("  const int64_t buf_bytes = (a.st1 - a.st0) * B;")
-        e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {max(SL // 8, 1)} * {NT} + tid;")
-        e(f"  for (int64_t tile = blockIdx.x; tile * {WPC} < nwin; tile += gridDim.x) {{")
+        e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {SQ} * {NT} + tid;")
+        e("  uint4* const wslot = slot - t;  // lane 0 of this window's lane group")
+        e("  uint4* const my_llr = s_llr + tid;")
+        e(f"  vt::Traceback<K, BL> tb;")
+        e("  tb.running = false;")
+        e("  tb.active = false;")
+        e("  int parity_prev = 0, parity = 0;")
+        # field address of (block, state) for a tile stored with `par`
+        e("  auto field_word = [&](int blk, uint32_t j, int par) -> const uint32_t* {")
+        e("    const int bs = blk - a.b_lo;")
+        e("    const int x = par ? (a.nbs - 1 - bs) : bs;")
+        if tau:
+            e(f"    const uint32_t tl = j >> {top}, r = j & {(1 << top) - 1};")
+        else:
+            e("    const uint32_t tl = 0, r = j;")
+        e(f"    const uint4* q = wslot + tl + ((size_t)x * {SQ} + (r >> 3)) * {NT};")
+        e("    return reinterpret_cast<const uint32_t*>(q) + ((r & 7) >> 1);")
+        e("  };")
+        e(f"  for (int64_t tile = blockIdx.x; tile * {WPC} < nwin; tile += gridDim.x, parity ^= 1) {{")
         e(f"    const int64_t wrel = tile * {WPC} + wloc;")
         e("    const bool active = wrel < nwin;")
-        e("    const vt::Window g = vt::window_geometry(a, a.w0 + (active ? wrel : nwin - 1));")
+        e("    const vt::Window g = vt::window_geometry<BL>(a, a.w0 + (active ? wrel : nwin - 1));")
         e("    const int64_t o0 = (g.g0 - a.st0) * B;")
-        e("    const int shift = (int)(o0 & 15);")
-        top = self.k - tau if tau else 0
         e("    " + " ".join(f"int32_t m{r} = 0;" for r in range(SL)))
         e("    int32_t rfold = 0;")
         e("    int64_t offset = 0;")
-        e("    uint4 raw[B + 1];")
-        e("    uint32_t cur[4 * B];")
-        e("    vt::load_raw<B>(raw, a.llr, buf_bytes, o0);")
-        e("    vt::realign<B>(cur, raw, shift, (int)min(max((g.s - g.g0) * B, (int64_t)0), (int64_t)16 * B));")
+        e("    uint32_t cur[NWC];")
+        e("    vt::stage_llr<NL, %d>(my_llr, a.llr, buf_bytes, o0, pol_first);" % NT)
+        e("    vt::cp_async_wait_all();")
+        e("    vt::realign<NL, NWC, %d>(cur, my_llr, (int)(o0 & 15), "
+          "(int)min(max((g.s - g.g0) * B, (int64_t)0), (int64_t)BL * B));" % NT)
         e("    for (int c = 0; c < a.nc; ++c) {")
-        e("      if (c + 1 < a.nc) vt::load_raw<B>(raw, a.llr, buf_bytes, o0 + (int64_t)16 * B * (c + 1));")
-        names, lo_end, xchg = self.block([f"m{r}" for r in range(SL)], top)
-        self.lo_end = lo_end
-        # block end: stream histories, clear them
+        e("      const int64_t on = o0 + (int64_t)BL * B * (c + 1);")
+        e("      if (c + 1 < a.nc) vt::stage_llr<NL, %d>(my_llr, a.llr, buf_bytes, on, pol_first);" % NT)
+        e("      // one traceback step of the previous tile; the field load overlaps this chunk's ACS")
+        e("      const bool tb_load = (t == 0) && tb.running && tb.b >= a.b_lo;")
+        e("      uint32_t tb_half = 0;")
+        e("      if (tb_load) {")
+        e("        const uint32_t* fw = field_word(tb.b, tb.j, parity_prev);")
+        if tau:
+            e(f"        tb_half = (tb.j & {(1 << top) - 1}) & 1;")
+        else:
+            e("        tb_half = tb.j & 1;")
+        e("        vt::cp_async4(&s_tb[tid], fw);")
+        e("      }")
+        e("      int32_t cmul = 1;")
+        e("#pragma unroll 1")
+        e(f"      for (int it = 0; it < {NIT}; ++it) {{")
+        self.body("        ")
+        self.shift_cur("        ")
+        e(f"        cmul <<= {P};")
+        e("        rfold = 0;")
+        e("      }")
+        e("      vt::cp_async_wait_all();")
+        e("      if (tb_load) tb.step(a, (s_tb[tid] >> (16 * tb_half)) & 0xFFFFu);")
+        # block end: histories (top partition) to scratch
         e("      if (c >= a.b_lo) {")
-        e(f"        uint4* const dst = slot + (size_t)(c - a.b_lo) * {max(SL // 8, 1)} * {NT};")
+        e("        const int bs = c - a.b_lo;")
+        e(f"        uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - bs) : bs) * {SQ} * {NT};")
         for gq in range(0, SL, 8):
             w = []
             for h in range(4):
                 ra, rb = gq + 2 * h, gq + 2 * h + 1
-                a_ = names[ra] if ra < SL else "0"
-                b_ = names[rb] if rb < SL else "0"
+                a_ = f"m{ra}" if ra < SL else "0"
+                b_ = f"m{rb}" if rb < SL else "0"
                 w.append(f"vt::prmt((uint32_t){a_}, (uint32_t){b_}, 0x5410u)")
-            e(f"        dst[{gq // 8} * {NT}] = make_uint4({', '.join(w)});")
-        if SL < 8:  # small codes: pad the single uint4 group
-            pass
+            e(f"        vt::st_global_v4_hint(dst + {gq // 8} * {NT}, make_uint4({', '.join(w)}), pol_last);")
         e("      }")
         for r in range(SL):
-            e(f"      const int32_t z{r} = {names[r]} & (int32_t)0xFFFF0000;")
+            e(f"      m{r} &= (int32_t)0xFFFF0000;")
         if T > 1:
-            e("      rfold = __shfl_sync(gmask, z0, lane0);")
+            e("      rfold = __shfl_sync(0xFFFFFFFFu, m0, lane0);")
         else:
-            e("      rfold = z0;")
+            e("      rfold = m0;")
         e("      if (c + 1 < a.nc) {")
-        if T > 1:
-            nxt = self.exchange([f"z{r}" for r in range(SL)], lo_end, tag="blk")
-            for r in range(SL):
-                e(f"        m{r} = {nxt[r]};")
-        else:
-            for r in range(SL):
-                e(f"        m{r} = z{r};")
         e("        offset += (rfold >> 16);")
-        e("        vt::realign<B>(cur, raw, shift, "
-          "(int)min(max((g.s - (g.g0 + 16 * (int64_t)(c + 1))) * B, (int64_t)0), (int64_t)16 * B));")
-        e("      } else {")
-        for r in range(SL):
-            e(f"        m{r} = z{r};")
+        e("        vt::realign<NL, NWC, %d>(cur, my_llr, (int)(on & 15), "
+          "(int)min(max((g.s - (g.g0 + (int64_t)BL * (c + 1))) * B, (int64_t)0), (int64_t)BL * B));" % NT)
         e("      }")
         e("    }")
-        # argmax (lowest index on ties): key = M | (S-1-j)
-        e(f"    // final state: argmax, lowest index on ties (reference.py:138); partition [{lo_end},{lo_end + tau})")
-        tsh = f"(t << {lo_end})" if tau else "0"
-        keys = []
-        for r in range(SL):
-            j0 = self.state_of(r, 0, lo_end)
-            keys.append(f"(m{r} | ({S - 1 - j0} - {tsh}))")
+        e("    if (t == 0 && tb.running) tb.drain_unstored(a);")
+        # argmax in the top partition: key = M | (S-1-j)
+        e("    // final state: argmax, lowest index on ties (reference.py:138)")
+        tsh = f"(t << {top})" if tau else "0"
+        keys = [f"(m{r} | ({S - 1 - self.state_of(r, 0, top)} - {tsh}))" for r in range(SL)]
         e(f"    int32_t best = {keys[0]};")
         for r in range(1, SL):
             e(f"    best = max(best, {keys[r]});")
-        if T > 1:
-            for d in range(tau):
-                e(f"    best = max(best, __shfl_xor_sync(gmask, best, {1 << d}));")
+        for d in range(tau):
+            e(f"    best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, {1 << d}));")
         e(f"    const uint32_t jst = (uint32_t)({S - 1} - (best & 0xFFFF));")
-        e(f"    if (t == 0 && active && a.final_metric) a.final_metric[wrel] = (int64_t)(best >> 16) + offset;")
-        # traceback (one lane per window)
-        e("    if (t == 0) {")
-        e(f"      uint4* const wslot = slot - t;  // lane 0 of this window")
-        e("      vt::traceback_emit<%d>(a, g, jst, active, [&](int bs, uint32_t j) -> uint32_t {" % K)
+        e("    if (t == 0 && active && a.final_metric) a.final_metric[wrel] = (int64_t)(best >> 16) + offset;")
+        e("    if (t == 0) tb.start(g, jst, active, a.nc);")
+        e("    parity_prev = parity;")
+        e("  }")
+        e("  // traceback of the CTA's last tile (no following tile to hide it behind)")
+        e("  if (t == 0) {")
+        e("    while (tb.running && tb.b >= a.b_lo) {")
+        e("      const uint32_t w = *field_word(tb.b, tb.j, parity_prev);")
         if tau:
-            e(f"        const uint32_t tl = (j >> {lo_end}) & {T - 1};")
-            e(f"        const uint32_t r = ((j >> {lo_end + tau}) << {lo_end}) | (j & {(1 << lo_end) - 1});")
+            e(f"      tb.step(a, (w >> (16 * ((tb.j & {(1 << top) - 1}) & 1))) & 0xFFFFu);")
         else:
-            e("        const uint32_t tl = 0, r = j;")
-        e(f"        const uint4* q = wslot + tl + ((size_t)bs * {max(SL // 8, 1)} + (r >> 3)) * {NT};")
-        e("        return (uint32_t)reinterpret_cast<const uint16_t*>(q)[r & 7];")
-        e("      });")
+            e("      tb.step(a, (w >> (16 * (tb.j & 1))) & 0xFFFFu);")
         e("    }")
+        e("    if (tb.running) tb.drain_unstored(a);")
         e("  }")
         e("}")
         e("")
@@ -294,7 +334,7 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
     codes = codes or STANDARD_CODES
     os.makedirs(outdir, exist_ok=True)
     files = []
-    reg = ["// GENERATED by gen_kernels.py -- kernel registry", ""]
+    reg = ["// GENERATED by gen_kernels.py -- kernel registry: VT_KERNEL(fn, K, B, T, SL, BL, {gens})", ""]
     decl = ["// GENERATED by gen_kernels.py -- kernel declarations", '#include "../vt_common.cuh"', ""]
     for name, (K, polys) in codes.items():
         gens = tuple(int(p, 8) for p in polys)
@@ -308,7 +348,7 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
         files.append(path)
         gl = ", ".join(f"{x}u" for x in gens)
         decl.append(f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);')
-        reg.append(f"VT_KERNEL(vtk_{name}, {K}, {len(gens)}, {T}, {g.SL}, {{{gl}}})")
+        reg.append(f"VT_KERNEL(vtk_{name}, {K}, {len(gens)}, {T}, {g.SL}, {g.BL}, {{{gl}}})")
     for fname, lines in (("registry.inc", reg), ("registry_decl.inc", decl)):
         rpath = os.path.join(outdir, fname)
         text = "\n".join(lines) + "\n"

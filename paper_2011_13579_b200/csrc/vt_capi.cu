@@ -33,13 +33,14 @@ struct Geometry {
   int nc, b_lo, nbs;
 };
 
-Geometry geometry(int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1) {
+Geometry geometry(int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1, int BL) {
+  // windows are cut into BL-stage history blocks aligned to the window end
   Geometry g;
   g.nwin = w1 - w0;
   const int64_t lmax = std::min<int64_t>(N, F + 2 * V);
-  g.nc = (int)((lmax + 15) / 16);
+  g.nc = (int)((lmax + BL - 1) / BL);
   const int64_t head = std::min<int64_t>(N, F + V);  // max (stop - emit_start) over windows
-  int64_t blo = (16 * (int64_t)g.nc - head) / 16;
+  int64_t blo = ((int64_t)BL * g.nc - head) / BL;     // first block any window needs for its emit range
   if (blo < 0) blo = 0;
   g.b_lo = (int)blo;
   g.nbs = g.nc - g.b_lo;
@@ -50,13 +51,12 @@ Geometry geometry(int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1) {
 // kernel registry: one generated kernel per supported code (gen/registry.inc)
 // ---------------------------------------------------------------------------
 struct KernelEntry {
-  int K, B, T, SL;
+  int K, B, T, SL, BL;
   uint32_t gens[VT_MAX_OUTPUTS];
   const void* fn;
 };
 
-#define VT_KERNEL(fn_, K_, B_, T_, SL_, ...) {K_, B_, T_, SL_, __VA_ARGS__, (const void*)&fn_},
-#define VT_DECL_ONLY
+#define VT_KERNEL(fn_, K_, B_, T_, SL_, BL_, ...) {K_, B_, T_, SL_, BL_, __VA_ARGS__, (const void*)&fn_},
 }  // namespace
 #include "gen/registry_decl.inc"
 namespace {
@@ -129,7 +129,7 @@ int vt_code_supported(const vt_code* code) { return find(code) != nullptr ? 1 : 
 size_t vt_workspace_bytes(const vt_code* code, int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1) {
   const KernelEntry* k = find(code);
   if (!k || N < 1 || F < 1 || V < 0 || w1 <= w0) return 0;
-  const Geometry g = geometry(N, F, V, w0, w1);
+  const Geometry g = geometry(N, F, V, w0, w1, k->BL);
   return scratch_bytes(k, g, grid_for(k, g.nwin));
 }
 
@@ -158,7 +158,7 @@ int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, 
     return fail(VT_EINVAL, "llr stage range [%lld, %lld) does not cover [%lld, %lld)", (long long)st0,
                 (long long)st1, (long long)need_lo, (long long)need_hi);
 
-  const Geometry g = geometry(N, F, V, w0, w1);
+  const Geometry g = geometry(N, F, V, w0, w1, k->BL);
   const int64_t grid = grid_for(k, g.nwin);
   const size_t need = scratch_bytes(k, g, grid);
   if (!workspace || workspace_bytes < need)

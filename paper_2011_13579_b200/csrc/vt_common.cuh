@@ -21,7 +21,7 @@ struct StreamArgs {
   uint32_t* bits;         // packed output bits of the whole stream (LSB = earliest, cli.py:5-6)
   int64_t* final_metric;  // optional, per window (index w - w0): max path metric (reference.py:206)
   uint4* scratch;         // survivor-history scratch: gridDim.x * nbs * (S/T/8) * NT uint4
-  int nc;                 // 16-stage chunks per window (uniform for the launch)
+  int nc;                 // BL-stage chunks per window (uniform for the launch; BL = kernel block length)
   int b_lo;               // first chunk whose histories are stored
   int nbs;                // stored chunks per window (nc - b_lo)
 };
@@ -39,6 +39,13 @@ __device__ __forceinline__ int32_t add_fma(int32_t a, int32_t b) {
   return d;
 }
 
+// a * b + c on the FMA pipe
+__device__ __forceinline__ int32_t mad_fma(int32_t a, int32_t b, int32_t c) {
+  int32_t d;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 // max(a + b, c): ptxas fuses add.s32 + max.s32 into one DPX VIADDMNMX (ALU pipe)
 __device__ __forceinline__ int32_t addmax(int32_t a, int32_t b, int32_t c) {
   int32_t d;
@@ -46,51 +53,82 @@ __device__ __forceinline__ int32_t addmax(int32_t a, int32_t b, int32_t c) {
   return d;
 }
 
+// --- asynchronous copies (cannot be sunk by the scheduler, unlike plain loads) ---
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 16-byte global->shared copy; src_bytes = 0 zero-fills (out-of-range words)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes, uint64_t pol) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(s), "l"(gmem),
+               "r"(src_bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void st_global_v4_hint(uint4* p, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+
 // Window geometry of window w (framing.py:78-82) in the end-aligned chunk frame.
 struct Window {
   int64_t e0, e1;   // emit range
   int64_t s, stop;  // window range
-  int64_t g0;       // stream stage of chunk 0 (= stop - 16*nc; may be < s: zero padding)
+  int64_t g0;       // stream stage of chunk 0 (= stop - BL*nc; may be < s: zero padding)
 };
 
+template <int BL>
 __device__ __forceinline__ Window window_geometry(const StreamArgs& a, int64_t w) {
   Window g;
   g.e0 = w * a.F;
   g.e1 = min(g.e0 + a.F, a.N);
   g.s = max((int64_t)0, g.e0 - a.V);
   g.stop = min(a.N, g.e1 + a.V);
-  g.g0 = g.stop - 16 * (int64_t)a.nc;
+  g.g0 = g.stop - BL * (int64_t)a.nc;
   return g;
 }
 
-// Load the 16-byte words covering LLR bytes [o, o + 16B) of the buffer (o may
-// be negative or run past the end: those words read as zero).
-template <int B>
-__device__ __forceinline__ void load_raw(uint4 (&raw)[B + 1], const int8_t* __restrict__ llr, int64_t buf_bytes,
-                                         int64_t o) {
+// Stage the 16-byte words covering LLR bytes [o, o + nb) of the buffer into
+// this thread's shared slot (column layout smem[i * NT + tid]); words outside
+// the buffer are zero-filled.  Completes at cp_async_wait_all().
+template <int NL, int NT>
+__device__ __forceinline__ void stage_llr(uint4* smem_col, const int8_t* __restrict__ llr, int64_t buf_bytes,
+                                          int64_t o, uint64_t pol) {
   const int64_t base = (o >> 4) << 4;  // floor to 16 (arithmetic shift)
 #pragma unroll
-  for (int i = 0; i <= B; ++i) {
+  for (int i = 0; i < NL; ++i) {
     const int64_t a = base + 16 * i;
-    if (a >= 0 && a < buf_bytes)
-      raw[i] = __ldg(reinterpret_cast<const uint4*>(llr + a));
-    else
-      raw[i] = make_uint4(0u, 0u, 0u, 0u);
+    const bool ok = (a >= 0) && (a < buf_bytes);
+    cp_async16(smem_col + i * NT, llr + (ok ? a : 0), ok ? 16 : 0, pol);
   }
 }
 
-// Realign raw words by the byte misalignment (0..15) into 4B words holding
-// bytes [o, o + 16B); zero the first `zb` bytes (stages before the window).
-template <int B>
-__device__ __forceinline__ void realign(uint32_t (&out)[4 * B], const uint4 (&raw)[B + 1], int shift, int zb) {
-  constexpr int NW = 4 * (B + 1);
+// Realign the staged words by the byte misalignment (o & 15) into NWC words
+// holding bytes [o, o + 4*NWC); zero the first `zb` bytes (stages before the window).
+template <int NL, int NWC, int NT>
+__device__ __forceinline__ void realign(uint32_t (&out)[NWC], const uint4* smem_col, int shift, int zb) {
+  constexpr int NW = 4 * NL;
+  static_assert(NWC + 4 <= NW, "staging window too small");
   uint32_t w[NW];
 #pragma unroll
-  for (int i = 0; i <= B; ++i) {
-    w[4 * i + 0] = raw[i].x;
-    w[4 * i + 1] = raw[i].y;
-    w[4 * i + 2] = raw[i].z;
-    w[4 * i + 3] = raw[i].w;
+  for (int i = 0; i < NL; ++i) {
+    const uint4 v = smem_col[i * NT];
+    w[4 * i + 0] = v.x;
+    w[4 * i + 1] = v.y;
+    w[4 * i + 2] = v.z;
+    w[4 * i + 3] = v.w;
   }
   const int q = shift >> 2, r = (shift & 3) * 8;
 #pragma unroll
@@ -98,10 +136,10 @@ __device__ __forceinline__ void realign(uint32_t (&out)[4 * B], const uint4 (&ra
 #pragma unroll
   for (int i = 0; i + 2 < NW; ++i) w[i] = (q & 2) ? w[i + 2] : w[i];
 #pragma unroll
-  for (int k = 0; k < 4 * B; ++k) out[k] = __funnelshift_r(w[k], w[k + 1], r);
+  for (int k = 0; k < NWC; ++k) out[k] = __funnelshift_r(w[k], w[k + 1], r);
   if (zb > 0) {
 #pragma unroll
-    for (int k = 0; k < 4 * B; ++k) {
+    for (int k = 0; k < NWC; ++k) {
       const int lo = zb - 4 * k;
       if (lo >= 4) out[k] = 0u;
       else if (lo > 0) out[k] &= 0xFFFFFFFFu << (8 * lo);
@@ -115,49 +153,77 @@ __device__ __forceinline__ int32_t llr_hi16(uint32_t word, uint32_t sh) {
   return (int32_t)prmt(word, 0u, ((8u | sh) << 12) | (sh << 8) | 0x44u);
 }
 
-// Traceback over the stored 16-stage survivor histories and packed emission of
+// Traceback over the stored BL-stage survivor histories and packed emission of
 // the window's emit range [e0, e1) (reference.py:131-144; framing.py:136-137).
-//   jst: final state (lowest-index argmax);  field(b, j) returns the 16-bit
-//   history of state j at the end of chunk b (decision of stage p in bit p).
-// Per chunk: bits = ((h | j << 16) >> (K-1)) & 0xFFFF, j = h & (S-1).
-template <int K, class FieldFn>
-__device__ __forceinline__ void traceback_emit(const StreamArgs& a, const Window& g, uint32_t jst, bool active,
-                                               FieldFn field) {
-  constexpr uint32_t S = 1u << (K - 1);
-  const int64_t top = ((g.e1 + 31) >> 5) << 5;
-  int64_t hiw = (g.e1 - 1) >> 5;
-  const int64_t loww = g.e0 >> 5;
-  int64_t lo = top;  // acc holds the decoded bits of stream positions [lo, (hiw + 1) * 32)
-  uint64_t acc = 0;
-  auto flush = [&]() {
+// A block's history h holds the decision of block stage p in bit p (newest
+// highest); from the state j at the block end:
+//   decoded bits of the block = ((h | j << BL) >> (K-1)) & (2^BL - 1)
+//   state before the block    = ((j << BL) | h) & (S-1)
+// The walk is a state machine so the kernel can interleave one step per
+// forward chunk of the next tile (the dependent field loads then hide behind
+// ACS work).
+template <int K, int BL>
+struct Traceback {
+  static constexpr uint32_t S = 1u << (K - 1);
+  int64_t e0, e1, g0, top, hiw, loww, lo;
+  uint64_t acc;
+  uint32_t j;
+  int b;         // next block (descending)
+  bool active;   // emits output (window exists)
+  bool running;  // words left to emit
+
+  __device__ __forceinline__ void start(const Window& g, uint32_t jst, bool act, int nc) {
+    e0 = g.e0;
+    e1 = g.e1;
+    g0 = g.g0;
+    top = ((g.e1 + 31) >> 5) << 5;
+    hiw = (g.e1 - 1) >> 5;
+    loww = g.e0 >> 5;
+    lo = top;
+    acc = 0;
+    j = jst;
+    b = nc - 1;
+    active = act;
+    running = hiw >= loww;
+  }
+
+  __device__ __forceinline__ void flush(const StreamArgs& a) {
     const int64_t wlo = hiw << 5, whi = wlo + 32;
     uint32_t word = (uint32_t)(wlo >= lo ? (acc >> (wlo - lo)) : (acc << (lo - wlo)));
-    const int64_t vlo = max(wlo, g.e0), vhi = min(whi, g.e1);
+    const int64_t vlo = max(wlo, e0), vhi = min(whi, e1);
     const uint32_t mask = (vhi - vlo >= 32) ? 0xFFFFFFFFu : (((1u << (vhi - vlo)) - 1u) << (vlo - wlo));
     word &= mask;
     if (active) {
-      const bool owned = (wlo >= g.e0) && (min(whi, a.N) <= g.e1);
+      const bool owned = (wlo >= e0) && (min(whi, a.N) <= e1);
       if (owned) a.bits[hiw] = word;
       else if (word) atomicOr(a.bits + hiw, word);
     }
     --hiw;
     const int64_t keep = ((hiw + 1) << 5) - lo;
     acc &= (keep >= 64) ? ~0ull : (keep > 0 ? ((1ull << keep) - 1ull) : 0ull);
-  };
-  for (int b = a.nc - 1; b >= 0 && hiw >= loww; --b) {
-    const int64_t gb = g.g0 + 16 * (int64_t)b;
-    const uint32_t h = (b >= a.b_lo) ? field(b - a.b_lo, jst) : 0u;
-    uint32_t bits16 = ((h | (jst << 16)) >> (K - 1)) & 0xFFFFu;
-    jst = h & (S - 1);
-    if (gb >= top) continue;
-    const int n_new = (int)(lo - gb);  // 16, or less for the block straddling `top`
-    if (n_new < 16) bits16 &= (1u << n_new) - 1u;
-    acc = (acc << n_new) | bits16;
-    lo = gb;
-    while (hiw >= loww && (hiw << 5) >= lo) flush();
   }
-  // words that start before the window's first chunk (only their in-window bits are kept)
-  while (hiw >= loww) flush();
-}
+
+  // consume block b with history h (0 for blocks that were not stored)
+  __device__ __forceinline__ void step(const StreamArgs& a, uint32_t h) {
+    const int64_t gb = g0 + BL * (int64_t)b;
+    uint32_t bits = (uint32_t)(((uint64_t)h | ((uint64_t)j << BL)) >> (K - 1)) & ((1u << BL) - 1u);
+    j = (uint32_t)(((uint64_t)j << BL) | h) & (S - 1);
+    --b;
+    if (gb >= top) return;
+    const int n_new = (int)(lo - gb);  // BL, or less for the block straddling `top`
+    if (n_new < BL) bits &= (1u << n_new) - 1u;
+    acc = (acc << n_new) | bits;
+    lo = gb;
+    while (hiw >= loww && (hiw << 5) >= lo) flush(a);
+    running = hiw >= loww;
+  }
+
+  // blocks below the stored range and words starting before the first chunk
+  __device__ __forceinline__ void drain_unstored(const StreamArgs& a) {
+    while (running && b >= 0) step(a, 0u);
+    while (hiw >= loww) flush(a);
+    running = false;
+  }
+};
 
 }  // namespace vt

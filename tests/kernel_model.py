@@ -1,10 +1,10 @@
 """Bit-level numpy model of the generated sm_100a kernel algorithm (test-only).
 
-It mirrors vt_common.cuh + gen_kernels.py step by step -- end-aligned 16-stage
+It mirrors vt_common.cuh + gen_kernels.py step by step -- end-aligned BL-stage
 chunks with zero-LLR front padding, int32 metrics M = lambda<<16 | history,
 +2^p on the i1 candidate, renormalisation folded into the first stage of a
-chunk, 16-bit history blocks, traceback j_prev = h & (S-1),
-bits = ((h | j<<16) >> (K-1)) & 0xFFFF -- so the design can be checked
+chunk, BL-bit history blocks, traceback j_prev = h & (S-1),
+bits = ((h | j<<BL) >> (K-1)) & (2^BL-1) -- so the design can be checked
 against the oracle on the CPU, independently of the CUDA code.
 """
 from __future__ import annotations
@@ -28,14 +28,17 @@ def _pattern_tables(K, gens):
     return S, i0, i1, pat(i0), pat(i1)
 
 
-def decode_stream_model(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> np.ndarray:
+def decode_stream_model(llr_nb: np.ndarray, K: int, gens, F: int, V: int, BL: int | None = None) -> np.ndarray:
+    """BL = history block length (defaults to the generated kernel's: (K-1)*floor(16/(K-1)))."""
+    if BL is None:
+        BL = (K - 1) * (16 // (K - 1))
     n, B = llr_nb.shape
     S, i0, i1, p0, p1 = _pattern_tables(K, gens)
     nw = -(-n // F)
     lmax = min(n, F + 2 * V)
-    nc = -(-lmax // 16)
+    nc = -(-lmax // BL)
     head = min(n, F + V)
-    b_lo = max(0, (16 * nc - head) // 16)
+    b_lo = max(0, (BL * nc - head) // BL)
     out = np.zeros(n, dtype=np.uint8)
     signs = np.array([[1 - 2 * ((p >> b) & 1) for b in range(B)] for p in range(1 << B)], dtype=np.int64)
     for w in range(nw):
@@ -43,13 +46,13 @@ def decode_stream_model(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> np.
         e1 = min(e0 + F, n)
         s = max(0, e0 - V)
         stop = min(n, e1 + V)
-        g0 = stop - 16 * nc
+        g0 = stop - BL * nc
         M = np.zeros(S, dtype=np.int64)
         rfold = 0
         fields = {}
         for c in range(nc):
-            for q in range(16):
-                st = g0 + 16 * c + q
+            for q in range(BL):
+                st = g0 + BL * c + q
                 ll = llr_nb[st].astype(np.int64) if st >= s else np.zeros(B, dtype=np.int64)
                 L = ll << 16
                 D = signs @ L - (rfold if q == 0 else 0)
@@ -65,14 +68,14 @@ def decode_stream_model(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> np.
         key = M | (S - 1 - np.arange(S))
         jst = S - 1 - (int(key.max()) & 0xFFFF)
         for b in range(nc - 1, -1, -1):
-            gb = g0 + 16 * b
+            gb = g0 + BL * b
             h = int(fields[b][jst]) if b in fields else 0
-            bits16 = ((h | (jst << 16)) >> (K - 1)) & 0xFFFF
-            jst = h & (S - 1)
-            for i in range(16):
+            bits = ((h | (jst << BL)) >> (K - 1)) & ((1 << BL) - 1)
+            jst = ((jst << BL) | h) & (S - 1)
+            for i in range(BL):
                 pos = gb + i
                 if e0 <= pos < e1:
-                    out[pos] = (bits16 >> i) & 1
+                    out[pos] = (bits >> i) & 1
             if gb <= e0:
                 break
     return out
