@@ -1,0 +1,84 @@
+"""Frame sharding across GPUs.
+
+Windows of ``plan_frames(N, F, V)`` are independent (framing.py:96-141:
+"Windows are independent; results do not depend on execution order"), so a
+stream shards over G ranks with no data exchange: rank g decodes the
+contiguous window range [w0, w1) from the stage range [st0, st1) (its emit
+ranges plus a V-stage halo each side) and writes a disjoint range of packed
+output words.  The only collective is an optional gather of the packed bits
+to one rank.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+__all__ = ["Shard", "shard_windows", "decode_stream_sharded", "gather_bits"]
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    w0: int  # first window (inclusive)
+    w1: int  # last window (exclusive)
+    st0: int  # first stage held by the rank's LLR buffer (multiple of 16)
+    st1: int  # one past the last stage held
+    word0: int  # first packed output word the rank completes
+    word1: int  # one past the last packed output word the rank completes
+
+    @property
+    def num_windows(self) -> int:
+        return self.w1 - self.w0
+
+
+def shard_windows(n: int, frame_len: int, overlap: int, world: int, rank: int) -> Shard:
+    """Contiguous, balanced window range of ``rank`` and the stage halo it needs."""
+    if n < 1 or frame_len < 1 or overlap < 0:
+        raise ValueError("bad stream geometry")
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    nw = -(-n // frame_len)
+    w0, w1 = nw * rank // world, nw * (rank + 1) // world
+    st0 = (max(0, w0 * frame_len - overlap) // 16) * 16
+    st1 = min(n, min(w1 * frame_len, n) + overlap) if w1 > w0 else st0
+    # words whose every bit is emitted by this rank's windows (boundary words may be shared)
+    e0, e1 = w0 * frame_len, min(w1 * frame_len, n)
+    word0 = -(-e0 // 32)
+    word1 = (n + 31) // 32 if w1 == nw else e1 // 32
+    return Shard(rank, w0, w1, st0, st1, word0, max(word0, word1))
+
+
+def decode_stream_sharded(llr_shard_nb, spec, n: int, frame_len: int, overlap: int, shard: Shard, out=None,
+                          stream=None):
+    """Decode this rank's windows from its int8 (st1-st0, B) device buffer.
+
+    Returns the packed int32 word tensor of the whole stream with this rank's
+    words filled (other words zero)."""
+    import ctypes
+
+    import torch
+
+    from ._lib import check, lib
+    from .decoder import _code, _ptr, _stream_ptr, _workspace
+
+    code = _code(spec)
+    nwords = (n + 31) // 32
+    if out is None:
+        out = torch.zeros(nwords, dtype=torch.int32, device=llr_shard_nb.device)
+    if shard.num_windows == 0:
+        return out
+    need = lib().vt_workspace_bytes(ctypes.byref(code), n, frame_len, overlap, shard.w0, shard.w1)
+    ws = _workspace(need)
+    check(lib().vt_decode_stream_range(ctypes.byref(code), _ptr(llr_shard_nb), shard.st0, shard.st1, n, frame_len,
+                                       overlap, shard.w0, shard.w1, _ptr(out), None, _ptr(ws), ws.numel(),
+                                       _stream_ptr(stream)))
+    return out
+
+
+def gather_bits(words, n: int, frame_len: int, overlap: int, group=None):
+    """OR-combine every rank's packed words onto all ranks (boundary words can
+    hold bits of two ranks, so a bitwise OR is the exact merge).  One
+    collective (all_reduce with BOR over int32 words); NCCL on GPUs, gloo on CPU."""
+    import torch.distributed as dist
+
+    dist.all_reduce(words, op=dist.ReduceOp.BOR, group=group)
+    return words
