@@ -108,6 +108,23 @@ int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N
                           uint32_t* bits_host, int8_t* llr_dev, uint32_t* bits_dev, void* workspace,
                           size_t workspace_bytes, int nchunks, void* stream);
 
+/* ---- BER harness (channel.py:69-99 of the reference) ---- */
+
+/* Synthetic AWGN/BPSK frames on the device: `frames` frames of frame_len
+ * info bits (Philox4x32-10 keyed by (seed, point)), encoded from the zero
+ * state per frame (codes.py:216-230), BPSK 0 -> +1, + sigma * N(0,1)
+ * (channel.py:76-87), quantised to int8 LLRs q = clamp(rint(llr_scale * y),
+ * -127, 127) (hard != 0: y >= 0 -> +1 else -1, reference.py:202-203).
+ * bits: packed info bits (ceil(frames*frame_len/32) words);
+ * llr: (frames*frame_len, B) int8, 4-byte aligned.  B must be 2..4. */
+int vt_channel_awgn(const vt_code* code, uint64_t seed, uint32_t point, int64_t frames, int64_t frame_len,
+                    float sigma, float llr_scale, int hard, uint32_t* bits, int8_t* llr, void* stream);
+
+/* Number of differing bits between two packed device bit vectors
+ * (channel.compute_ber, channel.py:90-99); *out is a device counter. */
+int vt_count_bit_errors(const uint32_t* a, const uint32_t* b, int64_t nwords, unsigned long long* out,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,7 +59,11 @@ def lib():
     L.vt_decode_frames.argtypes = [code_p, vp, i64, i64, vp, vp, vp, ctypes.c_size_t, vp]
     L.vt_decode_stream_host.argtypes = [code_p, vp, i64, i64, i64, vp, vp, vp, vp, ctypes.c_size_t,
                                         ctypes.c_int, vp]
-    for fn in ("vt_decode_stream", "vt_decode_stream_range", "vt_decode_frames", "vt_decode_stream_host"):
+    L.vt_channel_awgn.argtypes = [code_p, ctypes.c_uint64, ctypes.c_uint32, i64, i64, ctypes.c_float, ctypes.c_float,
+                                  ctypes.c_int, vp, vp, vp]
+    L.vt_count_bit_errors.argtypes = [vp, vp, i64, vp, vp]
+    for fn in ("vt_decode_stream", "vt_decode_stream_range", "vt_decode_frames", "vt_decode_stream_host",
+               "vt_channel_awgn", "vt_count_bit_errors"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L

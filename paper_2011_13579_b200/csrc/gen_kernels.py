@@ -75,9 +75,11 @@ class Gen:
         assert 1 << self.tau == T
         self.SL = self.S // T
         self.SQ = max(self.SL // 8, 1)  # uint4 groups of histories per lane per block
-        self.P = self.k - self.tau  # stages per loop body
-        self.NIT = 16 // self.P
-        self.BL = self.P * self.NIT  # history block length (stages)
+        self.P = self.k - self.tau  # stages per loop body (register naming / lane partition period)
+        self.NIT = 16 // self.P  # loop bodies per 16-stage history block
+        self.R = 16 - self.P * self.NIT  # tail stages after the loop (their naming permutation is
+        self.BL = 16  # absorbed by the block-end clears)
+        self.top = self.k - self.tau if self.tau else 0
         self.NL = self.B + 1  # staged 16-byte LLR words per block
         self.NWC = -(-self.BL * self.B // 4)  # realigned LLR words per block
         assert self.NWC + 4 <= 4 * self.NL
@@ -101,20 +103,21 @@ class Gen:
     def emit(self, s: str = ""):
         self.lines.append(s)
 
-    # -- loop body: P stages (+ exchange back to the top partition when T > 1) --
-    def body(self, ind: str) -> None:
-        B, P = self.B, self.P
-        top = self.k - self.tau if self.tau else 0
-        cur = [f"m{r}" for r in range(self.SL)]
-        lo = top
-        for q in range(P):
+    # -- one body of `n` stages ------------------------------------------------
+    def body(self, ind: str, n: int, names: list[str], lo: int, pfx: str, code_expr) -> tuple[list[str], int]:
+        """Emit n stages reading metrics `names` in partition `lo`.  code_expr(q)
+        returns the C expression of the history code added to the i1 candidate
+        at body stage q.  Returns (output names, output partition)."""
+        B = self.B
+        cur = list(names)
+        for q in range(n):
             lo_out = lo - 1 if self.tau else lo
             for b in range(B):
                 byte = q * B + b
                 expr = f"vt::llr_hi16(cur[{byte >> 2}], {byte & 3}u)"
                 if self.T > 1:
-                    expr = f"{expr} * f{q}_{b}"
-                self.emit(f"{ind}const int32_t L{q}_{b} = {expr};")
+                    expr = f"{expr} * f{self.top - lo}_{b}"
+                self.emit(f"{ind}const int32_t {pfx}L{q}_{b} = {expr};")
             body, need_d, need_e = [], set(), set()
             outs = []
             for r in range(self.SL):
@@ -128,30 +131,27 @@ class Gen:
                 p0, p1 = self.pattern(i0, u), self.pattern(i1, u)
                 need_d.add(p0)
                 need_e.add(p1)
-                nm = f"x{q}_{r}"
-                body.append(f"{ind}const int32_t {nm} = vt::addmax({cur[r0]}, D{q}_{p0}, "
-                            f"vt::add_fma({cur[r1]}, E{q}_{p1}));")
+                nm = f"{pfx}x{q}_{r}"
+                body.append(f"{ind}const int32_t {nm} = vt::addmax({cur[r0]}, {pfx}D{q}_{p0}, "
+                            f"vt::add_fma({cur[r1]}, {pfx}E{q}_{p1}));")
                 outs.append(nm)
             for p in sorted(need_d | need_e):
-                terms = [f"{'-' if (p >> b) & 1 else '+'} L{q}_{b}" for b in range(B)]
+                terms = [f"{'-' if (p >> b) & 1 else '+'} {pfx}L{q}_{b}" for b in range(B)]
                 expr = " ".join(terms).lstrip("+ ")
                 if q == 0:
                     expr = f"{expr} - rfold"
-                self.emit(f"{ind}const int32_t D{q}_{p} = {expr};")
-                if p in need_e:  # history code 2^(q + P*it) = (1 << q) * cmul, on the FMA pipe
-                    self.emit(f"{ind}const int32_t E{q}_{p} = vt::mad_fma(cmul, {1 << q}, D{q}_{p});")
+                self.emit(f"{ind}const int32_t {pfx}D{q}_{p} = {expr};")
+                if p in need_e:
+                    self.emit(f"{ind}const int32_t {pfx}E{q}_{p} = {code_expr(q, f'{pfx}D{q}_{p}')};")
             self.lines.extend(body)
             cur, lo = outs, lo_out
-        if self.T > 1:
-            cur = self.exchange(cur, lo, ind)
-        for r in range(self.SL):
-            self.emit(f"{ind}m{r} = {cur[r]};")
+        return cur, lo
 
-    def exchange(self, cur: list[str], lo: int, ind: str) -> list[str]:
+    def exchange(self, cur: list[str], lo: int, ind: str, tag: str = "") -> list[str]:
         """Shared-memory transpose from partition `lo` to the top-bit partition."""
         top = self.k - self.tau
         self.emit(f"{ind}// exchange: partition [{lo},{lo + self.tau}) -> [{top},{top + self.tau})")
-        self.emit(f"{ind}__syncwarp();")
+        self.emit(f"{ind}__syncwarp(gmask);")
         r = 0
         while r < self.SL:
             s0 = self.state_of(r, 0, lo)
@@ -165,10 +165,10 @@ class Gen:
             else:
                 self.emit(f"{ind}xw[{s0} + (t << {lo})] = {cur[r]};")
                 r += 1
-        self.emit(f"{ind}__syncwarp();")
+        self.emit(f"{ind}__syncwarp(gmask);")
         out = []
         for r in range(0, self.SL, 4):
-            nm = f"yx_{r}"
+            nm = f"yx{tag}_{r}"
             self.emit(f"{ind}const int4 {nm} = *reinterpret_cast<const int4*>(xr + {r});")
             out += [f"{nm}.x", f"{nm}.y", f"{nm}.z", f"{nm}.w"]
         return out
@@ -188,15 +188,17 @@ class Gen:
     # -- whole kernel ----------------------------------------------------------
     def kernel(self) -> str:
         K, B, S, SL, T, tau = self.K, self.B, self.S, self.SL, self.T, self.tau
-        BL, NL, NWC, SQ, P, NIT = self.BL, self.NL, self.NWC, self.SQ, self.P, self.NIT
+        BL, NL, NWC, SQ, P, NIT, R = self.BL, self.NL, self.NWC, self.SQ, self.P, self.NIT, self.R
         WPC = NT // T
         xstride = S + 4
-        top = self.k - tau if tau else 0
+        top = self.top
+        lo_end = top - R if tau else 0  # lane partition of the metrics at block end
+        self.lo_end = lo_end
         name = f"vtk_{self.name}"
         e = self.emit
         e("// GENERATED by gen_kernels.py -- do not edit.")
         e(f"// code {self.name}: K={K}, generators (octal) {', '.join(oct(g)[2:] for g in self.gens)}; "
-          f"{T} lane(s)/window, {SL} metrics/lane, {P}-stage body x {NIT} = {BL}-stage history blocks")
+          f"{T} lane(s)/window, {SL} metrics/lane; history block = {NIT} x {P}-stage loop body + {R}-stage tail")
         e('#include "../vt_common.cuh"')
         e("")
         e(f'extern "C" __global__ void __launch_bounds__({NT}, 1) {name}(const vt::StreamArgs a) {{')
@@ -211,6 +213,7 @@ class Gen:
             e(f"  int32_t* const xw = xs + wloc * {xstride};")
             e(f"  const int32_t* const xr = xw + (t << {top});")
             e("  const int lane0 = (tid & 31) & ~%d;" % (T - 1))
+            e(f"  const unsigned gmask = {(1 << T) - 1}u << lane0;  // this window's lanes (bodies may diverge per window)")
             for n in range(P):
                 lo_in = top - n
                 for b, g in enumerate(self.gens):
@@ -222,18 +225,21 @@ class Gen:
         e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {SQ} * {NT} + tid;")
         e("  uint4* const wslot = slot - t;  // lane 0 of this window's lane group")
         e("  uint4* const my_llr = s_llr + tid;")
-        e(f"  vt::Traceback<K, BL> tb;")
+        e("  vt::Traceback<K, BL> tb;")
         e("  tb.running = false;")
         e("  tb.active = false;")
         e("  int parity_prev = 0, parity = 0;")
-        # field address of (block, state) for a tile stored with `par`
-        e("  auto field_word = [&](int blk, uint32_t j, int par) -> const uint32_t* {")
+        # (lane, slot) of state j at block end, and the address of its history word
+        if tau:
+            tl_expr = f"(j >> {lo_end}) & {T - 1}"
+            r_expr = f"((j >> {lo_end + tau}) << {lo_end}) | (j & {(1 << lo_end) - 1})"
+        else:
+            tl_expr, r_expr = "0", "j"
+        e("  auto field_word = [&](int blk, uint32_t j, int par, uint32_t& half) -> const uint32_t* {")
         e("    const int bs = blk - a.b_lo;")
         e("    const int x = par ? (a.nbs - 1 - bs) : bs;")
-        if tau:
-            e(f"    const uint32_t tl = j >> {top}, r = j & {(1 << top) - 1};")
-        else:
-            e("    const uint32_t tl = 0, r = j;")
+        e(f"    const uint32_t tl = {tl_expr}, r = {r_expr};")
+        e("    half = r & 1;")
         e(f"    const uint4* q = wslot + tl + ((size_t)x * {SQ} + (r >> 3)) * {NT};")
         e("    return reinterpret_cast<const uint32_t*>(q) + ((r & 7) >> 1);")
         e("  };")
@@ -246,35 +252,45 @@ class Gen:
         e("    int32_t rfold = 0;")
         e("    int64_t offset = 0;")
         e("    uint32_t cur[NWC];")
-        e("    vt::stage_llr<NL, %d>(my_llr, a.llr, buf_bytes, o0, pol_first);" % NT)
+        e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole loop bodies of it")
+        e(f"    int it_start = (int)min(max(g.s - g.g0, (int64_t)0) / {P}, (int64_t){NIT});")
+        e(f"    const int64_t o0s = o0 + (int64_t)it_start * {P * B};")
+        e("    vt::stage_llr<NL, %d>(my_llr, a.llr, buf_bytes, o0s, pol_first);" % NT)
         e("    vt::cp_async_wait_all();")
-        e("    vt::realign<NL, NWC, %d>(cur, my_llr, (int)(o0 & 15), "
-          "(int)min(max((g.s - g.g0) * B, (int64_t)0), (int64_t)BL * B));" % NT)
+        e("    vt::realign<NL, NWC, %d>(cur, my_llr, (int)(o0s & 15), "
+          f"(int)min(max((g.s - g.g0 - (int64_t)it_start * {P}) * B, (int64_t)0), (int64_t)BL * B));" % NT)
         e("    for (int c = 0; c < a.nc; ++c) {")
         e("      const int64_t on = o0 + (int64_t)BL * B * (c + 1);")
         e("      if (c + 1 < a.nc) vt::stage_llr<NL, %d>(my_llr, a.llr, buf_bytes, on, pol_first);" % NT)
         e("      // one traceback step of the previous tile; the field load overlaps this chunk's ACS")
         e("      const bool tb_load = (t == 0) && tb.running && tb.b >= a.b_lo;")
         e("      uint32_t tb_half = 0;")
-        e("      if (tb_load) {")
-        e("        const uint32_t* fw = field_word(tb.b, tb.j, parity_prev);")
-        if tau:
-            e(f"        tb_half = (tb.j & {(1 << top) - 1}) & 1;")
-        else:
-            e("        tb_half = tb.j & 1;")
-        e("        vt::cp_async4(&s_tb[tid], fw);")
-        e("      }")
-        e("      int32_t cmul = 1;")
+        e("      if (tb_load) vt::cp_async4(&s_tb[tid], field_word(tb.b, tb.j, parity_prev, tb_half));")
+        e("      // history codes only in blocks whose decisions are stored (warm-up blocks need none)")
+        e("      const int32_t cflag = (c >= a.b_lo) ? 1 : 0;")
+        e(f"      int32_t cmul = cflag << ({P} * it_start);")
         e("#pragma unroll 1")
-        e(f"      for (int it = 0; it < {NIT}; ++it) {{")
-        self.body("        ")
+        e(f"      for (int it = it_start; it < {NIT}; ++it) {{")
+        names, lo = self.body("        ", P, [f"m{r}" for r in range(SL)], top, "",
+                              lambda q, d: f"vt::mad_fma(cmul, {1 << q}, {d})")
+        if T > 1:
+            names = self.exchange(names, lo, "        ", tag="b")
+        for r in range(SL):
+            e(f"        m{r} = {names[r]};")
         self.shift_cur("        ")
         e(f"        cmul <<= {P};")
         e("        rfold = 0;")
         e("      }")
+        e("      it_start = 0;")
+        fin = [f"m{r}" for r in range(SL)]
+        if R:
+            fin, lo = self.body("      ", R, fin, top, "t",
+                                lambda q, d: f"vt::mad_fma(cflag, {1 << (P * NIT + q)}, {d})")
+            assert lo == lo_end
+        e("      rfold = 0;")
         e("      vt::cp_async_wait_all();")
         e("      if (tb_load) tb.step(a, (s_tb[tid] >> (16 * tb_half)) & 0xFFFFu);")
-        # block end: histories (top partition) to scratch
+        # block end: histories to scratch, clear
         e("      if (c >= a.b_lo) {")
         e("        const int bs = c - a.b_lo;")
         e(f"        uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - bs) : bs) * {SQ} * {NT};")
@@ -282,28 +298,37 @@ class Gen:
             w = []
             for h in range(4):
                 ra, rb = gq + 2 * h, gq + 2 * h + 1
-                a_ = f"m{ra}" if ra < SL else "0"
-                b_ = f"m{rb}" if rb < SL else "0"
+                a_ = fin[ra] if ra < SL else "0"
+                b_ = fin[rb] if rb < SL else "0"
                 w.append(f"vt::prmt((uint32_t){a_}, (uint32_t){b_}, 0x5410u)")
             e(f"        vt::st_global_v4_hint(dst + {gq // 8} * {NT}, make_uint4({', '.join(w)}), pol_last);")
         e("      }")
         for r in range(SL):
-            e(f"      m{r} &= (int32_t)0xFFFF0000;")
+            e(f"      const int32_t z{r} = {fin[r]} & (int32_t)0xFFFF0000;")
         if T > 1:
-            e("      rfold = __shfl_sync(0xFFFFFFFFu, m0, lane0);")
+            e("      rfold = __shfl_sync(0xFFFFFFFFu, z0, lane0);")
         else:
-            e("      rfold = m0;")
+            e("      rfold = z0;")
         e("      if (c + 1 < a.nc) {")
+        if T > 1:
+            nxt = self.exchange([f"z{r}" for r in range(SL)], lo_end, "        ", tag="e")
+        else:
+            nxt = [f"z{r}" for r in range(SL)]
+        for r in range(SL):
+            e(f"        m{r} = {nxt[r]};")
         e("        offset += (rfold >> 16);")
         e("        vt::realign<NL, NWC, %d>(cur, my_llr, (int)(on & 15), "
           "(int)min(max((g.s - (g.g0 + (int64_t)BL * (c + 1))) * B, (int64_t)0), (int64_t)BL * B));" % NT)
+        e("      } else {")
+        for r in range(SL):
+            e(f"        m{r} = z{r};")
         e("      }")
         e("    }")
         e("    if (t == 0 && tb.running) tb.drain_unstored(a);")
-        # argmax in the top partition: key = M | (S-1-j)
+        # argmax in the block-end partition: key = M | (S-1-j)
         e("    // final state: argmax, lowest index on ties (reference.py:138)")
-        tsh = f"(t << {top})" if tau else "0"
-        keys = [f"(m{r} | ({S - 1 - self.state_of(r, 0, top)} - {tsh}))" for r in range(SL)]
+        tsh = f"(t << {lo_end})" if tau else "0"
+        keys = [f"(m{r} | ({S - 1 - self.state_of(r, 0, lo_end)} - {tsh}))" for r in range(SL)]
         e(f"    int32_t best = {keys[0]};")
         for r in range(1, SL):
             e(f"    best = max(best, {keys[r]});")
@@ -317,11 +342,9 @@ class Gen:
         e("  // traceback of the CTA's last tile (no following tile to hide it behind)")
         e("  if (t == 0) {")
         e("    while (tb.running && tb.b >= a.b_lo) {")
-        e("      const uint32_t w = *field_word(tb.b, tb.j, parity_prev);")
-        if tau:
-            e(f"      tb.step(a, (w >> (16 * ((tb.j & {(1 << top) - 1}) & 1))) & 0xFFFFu);")
-        else:
-            e("      tb.step(a, (w >> (16 * (tb.j & 1))) & 0xFFFFu);")
+        e("      uint32_t half;")
+        e("      const uint32_t w = *field_word(tb.b, tb.j, parity_prev, half);")
+        e("      tb.step(a, (w >> (16 * half)) & 0xFFFFu);")
         e("    }")
         e("    if (tb.running) tb.drain_unstored(a);")
         e("  }")

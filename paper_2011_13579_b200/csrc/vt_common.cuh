@@ -64,12 +64,12 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// 16-byte global->shared copy; src_bytes = 0 zero-fills (out-of-range words)
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes, uint64_t pol) {
+// 16-byte global->shared copy; src_bytes = 0 zero-fills (out-of-range words).
+// (No .L2::cache_hint operand: ptxas 12.9 allocated its 64-bit policy descriptor to
+// an odd uniform register in the K=9 kernels, which traps as an illegal instruction.)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes, uint64_t /*pol*/) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(s), "l"(gmem),
-               "r"(src_bytes), "l"(pol)
-               : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);

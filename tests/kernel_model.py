@@ -29,9 +29,9 @@ def _pattern_tables(K, gens):
 
 
 def decode_stream_model(llr_nb: np.ndarray, K: int, gens, F: int, V: int, BL: int | None = None) -> np.ndarray:
-    """BL = history block length (defaults to the generated kernel's: (K-1)*floor(16/(K-1)))."""
+    """BL = history block length (the generated kernels use 16)."""
     if BL is None:
-        BL = (K - 1) * (16 // (K - 1))
+        BL = 16
     n, B = llr_nb.shape
     S, i0, i1, p0, p1 = _pattern_tables(K, gens)
     nw = -(-n // F)
