@@ -108,6 +108,18 @@ int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N
                           uint32_t* bits_host, int8_t* llr_dev, uint32_t* bits_dev, void* workspace,
                           size_t workspace_bytes, int nchunks, void* stream);
 
+/* ---- paper-formulation tile decoder with the dragonfly permutation tie order ----
+ * matrix.decode_matrix_batch / decode_stream(decoder="matrix") with
+ * DecoderConfig(radix=4, optimized=True) (matrix.py:187-265, 306-334, 342-409):
+ * two-stage steps whose 4 candidates tie-break by priority prio[f*4 + x]
+ * (position of left-local state x of dragonfly f in its group
+ * representative's order; higher wins), a final radix-2 step for odd window
+ * lengths.  Same stream/window conventions as vt_decode_stream_range; K <= 9. */
+size_t vt_workspace_bytes_r4perm(const vt_code* code, int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1);
+int vt_decode_stream_r4perm(const vt_code* code, const uint8_t* prio, const int8_t* llr, int64_t st0, int64_t st1,
+                            int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1, uint32_t* bits,
+                            int64_t* final_metric, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- BER harness (channel.py:69-99 of the reference) ---- */
 
 /* Synthetic AWGN/BPSK frames on the device: `frames` frames of frame_len

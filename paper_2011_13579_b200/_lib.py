@@ -62,8 +62,12 @@ def lib():
     L.vt_channel_awgn.argtypes = [code_p, ctypes.c_uint64, ctypes.c_uint32, i64, i64, ctypes.c_float, ctypes.c_float,
                                   ctypes.c_int, vp, vp, vp]
     L.vt_count_bit_errors.argtypes = [vp, vp, i64, vp, vp]
+    L.vt_workspace_bytes_r4perm.argtypes = [code_p, i64, i64, i64, i64, i64]
+    L.vt_workspace_bytes_r4perm.restype = ctypes.c_size_t
+    L.vt_decode_stream_r4perm.argtypes = [code_p, vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, vp, vp,
+                                          ctypes.c_size_t, vp]
     for fn in ("vt_decode_stream", "vt_decode_stream_range", "vt_decode_frames", "vt_decode_stream_host",
-               "vt_channel_awgn", "vt_count_bit_errors"):
+               "vt_channel_awgn", "vt_count_bit_errors", "vt_decode_stream_r4perm"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L

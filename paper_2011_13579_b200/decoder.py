@@ -305,11 +305,19 @@ def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "referenc
         raise ValueError(f"unknown decoder {decoder!r}")
     if arr.shape[0] != spec.outputs_per_bit:
         raise ValueError("LLR input must have shape (B, N)")
+    r4perm = False
     if decoder == "matrix":
-        _check_matrix_config(spec, config or DecoderConfig())
+        cfg = config or DecoderConfig()
+        _, _, effective = _check_matrix_config(spec, cfg)
+        r4perm = cfg.radix == 4 and cfg.optimized and effective
     q = _as_int8_llr(arr).T.copy()  # (N, B) stage-major
     torch = _torch()
     n = q.shape[0]
+    if r4perm:  # radix-4 with the dragonfly permutation tie order (matrix.py:329-333)
+        dev = torch.from_numpy(q).cuda()
+        out = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev.device)
+        _decode_r4perm_device(dev, spec, n, plan.frame_len, plan.overlap, out)
+        return _unpack(out.cpu().numpy(), n)
     pinned = torch.from_numpy(q).pin_memory()
     words = decode_stream_host(pinned, spec, plan.frame_len, plan.overlap)
     return _unpack(words.numpy(), n)
@@ -394,29 +402,62 @@ def _check_matrix_config(spec: CodeSpec, config: DecoderConfig) -> tuple[int, in
                                   "exact integer metrics and does not reproduce it")
     t2 = _radix2_tiles(spec)
     t4, effective = (_radix4_tiles(spec, config.optimized) if config.radix == 4 else (0, False))
-    if config.radix == 4 and config.optimized and effective:
-        raise NotImplementedError("radix-4 with the dragonfly-group permutation (optimized=True) breaks ties in "
-                                  "permuted order (matrix.py:329-333); that tie order is not yet implemented "
-                                  "on sm_100a (use optimized=False, which is bit-identical to the reference)")
     return t2, t4, effective
+
+
+def _r4_priorities(spec: CodeSpec) -> np.ndarray:
+    """prio[f*4 + x]: position of left-local state x of dragonfly f in its group
+    representative's row order (matrix.py:237-241, 329-333): the radix-4
+    optimised path breaks ties toward the highest position."""
+    s4 = spec.num_states // 4
+    prio = np.tile(np.arange(4, dtype=np.uint8), s4)
+    for g in find_dragonfly_groups(2, spec):
+        for f, perm in g.permutations.items():
+            for i, x in enumerate(perm):
+                prio[f * 4 + x] = i
+    return prio
+
+
+def _decode_r4perm_device(llr_nb, spec: CodeSpec, n: int, frame_len: int, overlap: int, out, final_metric=None,
+                          stream=None):
+    code = _code(spec)
+    nw = -(-n // frame_len)
+    need = lib().vt_workspace_bytes_r4perm(ctypes.byref(code), n, frame_len, overlap, 0, nw)
+    ws = _workspace(need)
+    prio = np.ascontiguousarray(_r4_priorities(spec))
+    check(lib().vt_decode_stream_r4perm(ctypes.byref(code), prio.ctypes.data_as(ctypes.c_void_p), _ptr(llr_nb), 0,
+                                        n, n, frame_len, overlap, 0, nw, _ptr(out), _ptr(final_metric), _ptr(ws),
+                                        ws.numel(), _stream_ptr(stream)))
+    return out
 
 
 def decode_matrix_batch(llrs, spec: CodeSpec, config: DecoderConfig | None = None) -> MatrixDecodeResult:
     """matrix.decode_matrix_batch (matrix.py:342-386) on the B200 kernels.
 
     Radix-2 and radix-4 (non-optimised) decisions equal two-stage radix-2 ACS
-    with the natural tie rule, so the same exact
-    kernel serves both; the counter reports the paper's tile-op accounting."""
+    with the natural tie rule, so the fast kernel
+    serves both; radix-4 with an effective dragonfly-group optimisation breaks
+    ties in the representative's permuted order and runs on the r4perm kernel.
+    The counter reports the paper's tile-op accounting."""
     config = config or DecoderConfig()
     arr = np.asarray(llrs, dtype=np.float32)
     if arr.ndim != 3 or arr.shape[1] != spec.outputs_per_bit:
         raise ValueError("LLR batch must have shape (F, B, N)")
     f, _, n = arr.shape
-    t2, t4, _ = _check_matrix_config(spec, config)
+    t2, t4, effective = _check_matrix_config(spec, config)
     # matrix.py:290,320 (and 354-355): LLRs pass through binary16; exact for int8 values
     arr = arr.astype(np.float16).astype(np.float64)
     q = _as_int8_llr(arr)
-    bits, metric = _decode_frames_np(np.transpose(q, (0, 2, 1)), spec)
+    if config.radix == 4 and config.optimized and effective:
+        torch = _torch()
+        dev = torch.from_numpy(np.ascontiguousarray(np.transpose(q, (0, 2, 1)))).cuda().reshape(f * n, -1)
+        out = torch.zeros((f * n + 31) // 32, dtype=torch.int32, device=dev.device)
+        fm = torch.empty(f, dtype=torch.int64, device=dev.device)
+        _decode_r4perm_device(dev, spec, f * n, n, 0, out, fm)
+        bits = _unpack(out.cpu().numpy(), f * n).reshape(f, n)
+        metric = fm.cpu().numpy()
+    else:
+        bits, metric = _decode_frames_np(np.transpose(q, (0, 2, 1)), spec)
     counter = TileOpCounter()
     if config.radix == 2:
         counter.mma_ops = t2 * n

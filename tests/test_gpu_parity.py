@@ -64,10 +64,6 @@ def test_matrix_matches_reference_golden(vt, z, case):
     spec = _spec(vt, case["code"])
     cfg = vt.DecoderConfig(radix=case["radix"], optimized=case["optimized"], renormalize=case["renormalize"])
     llr = z[case["key"] + "_llr"].astype(np.float64)
-    if case["radix"] == 4 and case["optimized"] and case["code"] == "k7r2":
-        with pytest.raises(NotImplementedError):
-            vt.decode_matrix_batch(llr, spec, cfg)
-        return
     res = vt.decode_matrix_batch(llr, spec, cfg)
     np.testing.assert_array_equal(res.bits, z[case["key"] + "_bits"])
     np.testing.assert_array_equal(res.final_metric, z[case["key"] + "_metric"])
@@ -77,6 +73,21 @@ def test_matrix_matches_reference_golden(vt, z, case):
 
 @pytest.mark.parametrize("code", ["k7r2", "k7r3", "k9r2", "k8r2", "k5r2"])
 @pytest.mark.parametrize("fv", [(256, 42), (64, 20), (1000, 100), (37, 5), (256, 0)])
+def test_matrix_r4_optimized_stream_matches_reference_semantics(vt):
+    """decode_stream(decoder="matrix", radix-4 optimised) on a noisy stream: windows are
+    decoded independently, so it must equal decode_matrix_batch on each window."""
+    spec = vt.default_spec()
+    cfg = vt.DecoderConfig(radix=4, optimized=True)
+    _, q = oracle.synthetic_stream(3000, 7, (0o171, 0o133), ebn0_db=1.0, seed=5, scale=4.0)  # tie-heavy
+    plan = vt.plan_frames(3000, 256, 43)  # odd window lengths exercise the final radix-2 step
+    got = vt.decode_stream(q.T.astype(float), spec, plan, decoder="matrix", config=cfg)
+    want = np.zeros(3000, dtype=np.uint8)
+    for w in plan.windows:
+        bits = vt.decode_matrix_batch(q[w.start:w.stop].T[None].astype(float), spec, cfg).bits[0]
+        want[w.emit_start:w.emit_stop] = bits[w.emit_start - w.start:w.emit_stop - w.start]
+    np.testing.assert_array_equal(got, want)
+
+
 def test_random_streams_match_oracle(vt, code, fv):
     k, gens = code_params(CODES, code)
     spec = vt.CodeSpec(k, gens)
