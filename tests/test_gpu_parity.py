@@ -71,8 +71,6 @@ def test_matrix_matches_reference_golden(vt, z, case):
     assert (res.counter.mma_ops, res.counter.survivor_write_passes, res.counter.stages) == tuple(int(x) for x in c)
 
 
-@pytest.mark.parametrize("code", ["k7r2", "k7r3", "k9r2", "k8r2", "k5r2"])
-@pytest.mark.parametrize("fv", [(256, 42), (64, 20), (1000, 100), (37, 5), (256, 0)])
 def test_matrix_r4_optimized_stream_matches_reference_semantics(vt):
     """decode_stream(decoder="matrix", radix-4 optimised) on a noisy stream: windows are
     decoded independently, so it must equal decode_matrix_batch on each window."""
@@ -88,6 +86,8 @@ def test_matrix_r4_optimized_stream_matches_reference_semantics(vt):
     np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("code", ["k7r2", "k7r3", "k9r2", "k8r2", "k5r2"])
+@pytest.mark.parametrize("fv", [(256, 42), (64, 20), (1000, 100), (37, 5), (256, 0)])
 def test_random_streams_match_oracle(vt, code, fv):
     k, gens = code_params(CODES, code)
     spec = vt.CodeSpec(k, gens)
