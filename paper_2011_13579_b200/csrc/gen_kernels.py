@@ -80,6 +80,8 @@ class Gen:
         self.R = 16 - self.P * self.NIT  # tail stages after the loop (their naming permutation is
         self.BL = 16  # absorbed by the block-end clears)
         self.top = self.k - self.tau if self.tau else 0
+        self.G = (1 << self.top) + 32 // T if T > 1 else 0  # exchange buffer: lane-group stride (words)
+        self.XS = T * self.G + 4 if T > 1 else 0  # exchange buffer: window stride (words)
         self.NL = self.B + 1  # staged 16-byte LLR words per block
         self.NWC = -(-self.BL * self.B // 4)  # realigned LLR words per block
         assert self.NWC + 4 <= 4 * self.NL
@@ -148,22 +150,29 @@ class Gen:
         return cur, lo
 
     def exchange(self, cur: list[str], lo: int, ind: str, tag: str = "") -> list[str]:
-        """Shared-memory transpose from partition `lo` to the top-bit partition."""
+        """Shared-memory transpose from partition `lo` to the top-bit partition.
+        Layout per window: lane group g = s >> top at offset g*G, G = 2^top + 32/T
+        words, window stride XS = T*G + 4: the row reads (LDS.128) and the
+        body-exchange scalar writes are bank-conflict-free."""
         top = self.k - self.tau
+        G = self.G
+        assert lo + self.tau <= top
         self.emit(f"{ind}// exchange: partition [{lo},{lo + self.tau}) -> [{top},{top + self.tau})")
         self.emit(f"{ind}__syncwarp(gmask);")
+        lowmask = (1 << top) - 1
         r = 0
         while r < self.SL:
             s0 = self.state_of(r, 0, lo)
             run = 1
             while r + run < self.SL and self.state_of(r + run, 0, lo) == s0 + run and run < 4:
                 run += 1
-            if run == 4 and s0 % 4 == 0:
-                self.emit(f"{ind}*reinterpret_cast<int4*>(xw + {s0} + (t << {lo})) = "
+            off = (s0 & lowmask) + G * (s0 >> top)
+            if run == 4 and off % 4 == 0:
+                self.emit(f"{ind}*reinterpret_cast<int4*>(xw + {off} + (t << {lo})) = "
                           f"make_int4({cur[r]}, {cur[r + 1]}, {cur[r + 2]}, {cur[r + 3]});")
                 r += 4
             else:
-                self.emit(f"{ind}xw[{s0} + (t << {lo})] = {cur[r]};")
+                self.emit(f"{ind}xw[{off} + (t << {lo})] = {cur[r]};")
                 r += 1
         self.emit(f"{ind}__syncwarp(gmask);")
         out = []
@@ -190,7 +199,7 @@ class Gen:
         K, B, S, SL, T, tau = self.K, self.B, self.S, self.SL, self.T, self.tau
         BL, NL, NWC, SQ, P, NIT, R = self.BL, self.NL, self.NWC, self.SQ, self.P, self.NIT, self.R
         WPC = NT // T
-        xstride = S + 4
+        xstride = self.XS
         top = self.top
         lo_end = top - R if tau else 0  # lane partition of the metrics at block end
         self.lo_end = lo_end
@@ -211,7 +220,7 @@ class Gen:
         if T > 1:
             e(f"  __shared__ __align__(16) int32_t xs[{WPC} * {xstride}];")
             e(f"  int32_t* const xw = xs + wloc * {xstride};")
-            e(f"  const int32_t* const xr = xw + (t << {top});")
+            e(f"  const int32_t* const xr = xw + t * {self.G};")
             e("  const int lane0 = (tid & 31) & ~%d;" % (T - 1))
             e(f"  const unsigned gmask = {(1 << T) - 1}u << lane0;  // this window's lanes (bodies may diverge per window)")
             for n in range(P):
