@@ -366,7 +366,9 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
     codes = codes or STANDARD_CODES
     os.makedirs(outdir, exist_ok=True)
     files = []
-    reg = ["// GENERATED by gen_kernels.py -- kernel registry: VT_KERNEL(fn, K, B, T, SL, BL, {gens})", ""]
+    reg = ["// GENERATED by gen_kernels.py -- kernel registry:",
+           "// VT_KERNEL(fn, K, B, lanes/window T, windows/thread, SL, chunk CH, history group BL, uint4/group SQ, {gens})",
+           ""]
     decl = ["// GENERATED by gen_kernels.py -- kernel declarations", '#include "../vt_common.cuh"', ""]
     for name, (K, polys) in codes.items():
         gens = tuple(int(p, 8) for p in polys)
@@ -380,7 +382,23 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
         files.append(path)
         gl = ", ".join(f"{x}u" for x in gens)
         decl.append(f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);')
-        reg.append(f"VT_KERNEL(vtk_{name}, {K}, {len(gens)}, {T}, {g.SL}, {g.BL}, {{{gl}}})")
+        reg.append(f"VT_KERNEL(vtk_{name}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, {g.SQ}, {{{gl}}})")
+        if K == 7:  # packed 16x2 variant: two windows per thread
+            import sys
+            here = os.path.dirname(os.path.abspath(__file__))
+            if here not in sys.path:
+                sys.path.insert(0, here)
+            from gen_kernels16 import Gen16
+            g16 = Gen16(name, K, gens)
+            src16 = g16.kernel()
+            path16 = os.path.join(outdir, f"vtk16_{name}.cu")
+            if not os.path.exists(path16) or open(path16).read() != src16:
+                with open(path16, "w") as fh:
+                    fh.write(src16)
+            files.append(path16)
+            decl.append(f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a);')
+            reg.append(f"VT_KERNEL(vtk16_{name}, {K}, {len(gens)}, 1, 2, {g16.S}, {g16.CH}, {g16.L}, "
+                       f"{g16.S // 16}, {{{gl}}})")
     for fname, lines in (("registry.inc", reg), ("registry_decl.inc", decl)):
         rpath = os.path.join(outdir, fname)
         text = "\n".join(lines) + "\n"

@@ -1,0 +1,307 @@
+#!/usr/bin/env python3
+"""Generator for the packed 16x2 ACS kernels (two windows per thread), K <= 7.
+
+Each 32-bit register m_j holds the metric of state j for TWO windows: window
+A in the low 16 bits, window B in the high 16 bits.  Both windows walk the
+same trellis, so one `VIADD.16x2` (candidate i1) + one `VIADDMNMX.U16x2`
+(fused add of candidate i0 + unsigned max) advance state j of both windows:
+half the issue slots per state update of the s32 kernels (gen_kernels.py),
+the instruction pair `tools/pipe_bench.cu` measures at 101 state
+updates/cycle/SM.
+
+Per 16-bit half:  U = Lambda * 2^L + h  (unsigned), where
+  * h (L bits) records the survivor decisions of the current L-stage history
+    group (candidate i1 carries +2^q at group stage q, so unsigned max applies
+    the reference tie rule take1 = cand1 >= cand0, reference.py:121);
+  * Lambda is the biased path metric: every LLR term enters as l+128 or 128-l
+    (both >= 0), so each stage adds delta + 128*B >= 0; at each group start the
+    metrics are renormalised by Lambda_0 - S_b (S_b = 2(K-1)*128*B bounds the
+    metric spread), keeping Lambda in [0, 2*S_b + L*256*B] < 2^(16-L) (L = 3 for
+    K=7 r1/2, 2 for K=7 r1/3).  Per-half arithmetic is modular; the true values
+    stay in range, so the unsigned max is exact.
+At each group end the L-bit fields are masked out, packed 4 states per word
+(12 bits per half), streamed to the scratch slot and cleared.  The traceback
+walks groups: j_prev = ((j << L) | h) & (S-1), decoded bits =
+(j >> (K-1-L)) & (2^L - 1) (vt_common.cuh Traceback<K, L>).
+"""
+from __future__ import annotations
+
+from gen_kernels import NT, parity
+
+CH_BODIES = 2  # loop bodies per LLR chunk
+
+
+def history_bits(K: int, B: int) -> int:
+    dmax = 128 * B
+    sb = 2 * (K - 1) * dmax
+    for L in (6, 3, 2, 1):
+        if (K - 1) % L == 0 and 2 * sb + L * 2 * dmax < (1 << (16 - L)):
+            return L
+    raise ValueError("no history width fits")
+
+
+class Gen16:
+    def __init__(self, name: str, K: int, gens: tuple[int, ...]):
+        self.name = name
+        self.K = K
+        self.k = K - 1
+        self.S = 1 << self.k
+        assert self.S >= 16, "16x2 kernels pack 16 states per uint4 of history words"
+        self.gens = gens
+        self.B = len(gens)
+        self.L = history_bits(K, self.B)
+        self.P = self.k  # body length: the state->register naming returns to the identity
+        self.CH = self.P * CH_BODIES  # LLR chunk (stages)
+        self.GPB = self.P // self.L  # history groups per body
+        self.dmax = 128 * self.B
+        self.Sb = 2 * self.k * self.dmax
+        self.NWC = -(-self.CH * self.B // 4)
+        self.NL = -(-(self.NWC * 4 + 15) // 16)
+        while self.NWC + 4 > 4 * self.NL:
+            self.NL += 1
+        self.lines: list[str] = []
+
+    def pattern(self, i: int, u: int) -> int:
+        reg = (u << self.k) | i
+        return sum(parity(g & reg) << b for b, g in enumerate(self.gens))
+
+    def emit(self, s: str = "") -> None:
+        self.lines.append(s)
+
+    def stage(self, ind: str, q: int, names: list[str]) -> list[str]:
+        """One radix-2 stage (body position q) for both windows."""
+        B, L, S = self.B, self.L, self.S
+        gq = q % L
+        flag = f"cflag{q - gq}"
+        e = self.emit
+        for b in range(B):
+            byte = q * B + b
+            w, k = byte >> 2, byte & 3
+            sel = k | ((8 | k) << 4) | ((4 + k) << 8) | ((12 + k) << 12)
+            # (l_A, l_B) as signed 16-bit halves -> U = (l + 128) << L, N = (128 - l) << L, both >= 0
+            e(f"{ind}const uint32_t P{q}_{b} = vt::prmt(curA[{w}], curB[{w}], {sel:#x}u);")
+            e(f"{ind}const uint32_t U{q}_{b} = vt::vadd2(P{q}_{b}, 0x00800080u) << {L};")
+            e(f"{ind}const uint32_t N{q}_{b} = {(256 << L) * 0x10001:#x}u - U{q}_{b};")
+        outs, body, need_d, need_e = [], [], set(), set()
+        for j in range(S):
+            u = j >> (self.k - 1)
+            i0 = (j << 1) & (S - 1)
+            i1 = i0 | 1
+            p0, p1 = self.pattern(i0, u), self.pattern(i1, u)
+            need_d.add(p0)
+            need_e.add(p1)
+            nm = f"x{q}_{j}"
+            body.append(f"{ind}const uint32_t {nm} = vt::vaddmax2({names[i0]}, D{q}_{p0}, "
+                        f"vt::vadd2({names[i1]}, E{q}_{p1}));")
+            outs.append(nm)
+        for p in sorted(need_d | need_e):
+            expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(B))
+            if gq == 0:
+                expr = f"vt::vadd2({expr}, negR)"
+            e(f"{ind}const uint32_t D{q}_{p} = {expr};")
+            if p in need_e:
+                e(f"{ind}const uint32_t E{q}_{p} = vt::vadd2(D{q}_{p}, {flag} * {(1 << gq) * 0x10001:#x}u);")
+        self.lines.extend(body)
+        return outs
+
+    def group_end(self, ind: str) -> None:
+        """Traceback steps, history fields -> scratch + clear, renormalisation."""
+        L, S = self.L, self.S
+        e = self.emit
+        hm = ((1 << L) - 1) * 0x10001
+        lm = (0xFFFF & ~((1 << L) - 1)) * 0x10001
+        fm = (1 << L) - 1
+        e(f"{ind}// ---- group end")
+        e(f"{ind}vt::cp_async_wait_all();")
+        e(f"{ind}if (tbA_load) tbA.step(a, (s_tb[tid] >> tb_shA) & {fm}u);")
+        e(f"{ind}if (tbB_load) tbB.step(a, (s_tb[{NT} + tid] >> tb_shB) & {fm}u);")
+        e(f"{ind}if (gidx >= a.b_lo) {{")
+        e(f"{ind}  const int gs = gidx - a.b_lo;")
+        e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {S // 16} * {NT};")
+        for j in range(S):
+            e(f"{ind}  const uint32_t h{j} = m{j} & {hm:#x}u;")
+        words = []
+        for w in range(S // 4):
+            acc = f"h{4 * w}"
+            for t in range(1, 4):
+                acc = f"vt::mad_u32(h{4 * w + t}, {1 << (L * t)}u, {acc})"
+            words.append(acc)
+        for g in range(S // 16):
+            ws = ", ".join(words[4 * g: 4 * g + 4])
+            e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), pol_last);")
+        for j in range(S):
+            e(f"{ind}  m{j} = vt::mad_u32(h{j}, 0xFFFFFFFFu, m{j});")
+        e(f"{ind}}}")
+        e(f"{ind}++gidx;")
+        e(f"{ind}tbA_load = tbA.running && tbA.b >= a.b_lo;")
+        e(f"{ind}tbB_load = tbB.running && tbB.b >= a.b_lo;")
+        e(f"{ind}if (tbA_load) vt::cp_async4(&s_tb[tid], field_word(tbA.b, tbA.j, parity_prev, tb_shA));")
+        e(f"{ind}if (tbB_load) {{")
+        e(f"{ind}  vt::cp_async4(&s_tb[{NT} + tid], field_word(tbB.b, tbB.j, parity_prev, tb_shB));")
+        e(f"{ind}  tb_shB += 16;")
+        e(f"{ind}}}")
+        e(f"{ind}// renormalise the next group by Lambda_0 - S_b (per window half)")
+        e(f"{ind}offA += pendA;")
+        e(f"{ind}offB += pendB;")
+        e(f"{ind}{{")
+        e(f"{ind}  const uint32_t r0 = m0 & {lm:#x}u;")
+        e(f"{ind}  const uint32_t rr = vt::vadd2(r0, {((-(self.Sb << L)) & 0xFFFF) * 0x10001:#x}u);")
+        e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);")
+        e(f"{ind}  pendA = (int64_t)((r0 & 0xFFFFu) >> {L}) - {self.Sb};")
+        e(f"{ind}  pendB = (int64_t)(r0 >> {16 + L}) - {self.Sb};")
+        e(f"{ind}}}")
+
+    def shift_cur(self, ind: str) -> None:
+        nb = self.P * self.B
+        qw, rb = nb // 4, nb % 4
+        for arr in ("curA", "curB"):
+            for i in range(self.NWC):
+                a = f"{arr}[{i + qw}]" if i + qw < self.NWC else "0u"
+                if rb == 0:
+                    self.emit(f"{ind}{arr}[{i}] = {a};")
+                else:
+                    b = f"{arr}[{i + qw + 1}]" if i + qw + 1 < self.NWC else "0u"
+                    self.emit(f"{ind}{arr}[{i}] = __funnelshift_r({a}, {b}, {8 * rb});")
+
+    def kernel(self) -> str:
+        K, B, S, L, P, CH, NL, NWC = self.K, self.B, self.S, self.L, self.P, self.CH, self.NL, self.NWC
+        SQ = S // 16  # uint4 of history words per group per thread
+        name = f"vtk16_{self.name}"
+        e = self.emit
+        e("// GENERATED by gen_kernels16.py -- do not edit.")
+        e(f"// code {self.name}: K={K}, generators (octal) {', '.join(oct(g)[2:] for g in self.gens)}; "
+          f"two windows per thread (16x2 halves), {L}-bit history groups, {P}-stage body, {CH}-stage chunks")
+        e('#include "../vt_common.cuh"')
+        e("")
+        e(f'extern "C" __global__ void __launch_bounds__({NT}, 1) {name}(const vt::StreamArgs a) {{')
+        e(f"  constexpr int B = {B}, K = {K}, CH = {CH}, NL = {NL}, NWC = {NWC};")
+        e("  const int tid = threadIdx.x;")
+        e(f"  __shared__ __align__(16) uint4 s_llr[2 * NL * {NT}];")
+        e(f"  __shared__ uint32_t s_tb[2 * {NT}];")
+        e("  const uint64_t pol_last = vt::policy_evict_last();")
+        e("  const int64_t nwin = a.w1 - a.w0;")
+        e("  const int64_t buf_bytes = (a.st1 - a.st0) * B;")
+        e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {SQ} * {NT} + tid;")
+        e("  uint4* const llrA = s_llr + tid;")
+        e(f"  uint4* const llrB = s_llr + NL * {NT} + tid;")
+        e(f"  vt::Traceback<K, {L}> tbA, tbB;")
+        e("  tbA.running = tbB.running = false;")
+        e("  tbA.active = tbB.active = false;")
+        e("  int parity_prev = 0, parity = 0;")
+        e("  auto field_word = [&](int grp, uint32_t j, int par, uint32_t& sh) -> const uint32_t* {")
+        e("    const int gs = grp - a.b_lo;")
+        e("    const int x = par ? (a.nbs - 1 - gs) : gs;")
+        e(f"    sh = {L} * (j & 3);")
+        e(f"    const uint4* q = slot + ((size_t)x * {SQ} + (j >> 4)) * {NT};")
+        e("    return reinterpret_cast<const uint32_t*>(q) + ((j >> 2) & 3);")
+        e("  };")
+        e(f"  const int ng = a.nc * {CH // L};  // history groups per window")
+        e(f"  for (int64_t tile = blockIdx.x; tile * {2 * NT} < nwin; tile += gridDim.x, parity ^= 1) {{")
+        e(f"    const int64_t wa = tile * {2 * NT} + 2 * tid, wb = wa + 1;")
+        e("    const bool actA = wa < nwin, actB = wb < nwin;")
+        e(f"    const vt::Window gA = vt::window_geometry<{CH}>(a, a.w0 + (actA ? wa : nwin - 1));")
+        e(f"    const vt::Window gB = vt::window_geometry<{CH}>(a, a.w0 + (actB ? wb : nwin - 1));")
+        e("    const int64_t oA = (gA.g0 - a.st0) * B, oB = (gB.g0 - a.st0) * B;")
+        e("    " + " ".join(f"uint32_t m{j} = 0;" for j in range(S)))
+        e("    uint32_t negR = 0;")
+        e("    int64_t offA = 0, offB = 0, pendA = 0, pendB = 0;")
+        e("    uint32_t curA[NWC], curB[NWC];")
+        e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole bodies of it")
+        e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
+          f"(int64_t){CH_BODIES});")
+        e("    int it_start = it0;")
+        e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
+        e(f"    vt::stage_llr<NL, {NT}>(llrA, a.llr, buf_bytes, oA0, 0);")
+        e(f"    vt::stage_llr<NL, {NT}>(llrB, a.llr, buf_bytes, oB0, 0);")
+        e("    vt::cp_async_wait_all();")
+        e(f"    vt::realign<NL, NWC, {NT}>(curA, llrA, (int)(oA0 & 15), "
+          f"(int)min(max((gA.s - gA.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
+        e(f"    vt::realign<NL, NWC, {NT}>(curB, llrB, (int)(oB0 & 15), "
+          f"(int)min(max((gB.s - gB.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
+        e(f"    int gidx = it0 * {self.GPB};")
+        e("    // traceback of the previous tile: one group step per forward group, loads one group ahead")
+        e("    uint32_t tb_shA = 0, tb_shB = 0;")
+        e("    bool tbA_load = tbA.running && tbA.b >= a.b_lo;")
+        e("    bool tbB_load = tbB.running && tbB.b >= a.b_lo;")
+        e("    if (tbA_load) vt::cp_async4(&s_tb[tid], field_word(tbA.b, tbA.j, parity_prev, tb_shA));")
+        e("    if (tbB_load) {")
+        e(f"      vt::cp_async4(&s_tb[{NT} + tid], field_word(tbB.b, tbB.j, parity_prev, tb_shB));")
+        e("      tb_shB += 16;")
+        e("    }")
+        e("    for (int c = 0; c < a.nc; ++c) {")
+        e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
+        e("      if (c + 1 < a.nc) {")
+        e(f"        vt::stage_llr<NL, {NT}>(llrA, a.llr, buf_bytes, onA, 0);")
+        e(f"        vt::stage_llr<NL, {NT}>(llrB, a.llr, buf_bytes, onB, 0);")
+        e("      }")
+        e("#pragma unroll 1")
+        e(f"      for (int it = it_start; it < {CH_BODIES}; ++it) {{")
+        names = [f"m{j}" for j in range(S)]
+        for q in range(P):
+            if q % L == 0:
+                e("        // history codes only in groups whose decisions are stored (warm-up needs none)")
+                e(f"        const uint32_t cflag{q} = (gidx >= a.b_lo) ? 1u : 0u;")
+            names = self.stage("        ", q, names)
+            if q % L == L - 1:
+                for j in range(S):
+                    e(f"        m{j} = {names[j]};")
+                names = [f"m{j}" for j in range(S)]
+                self.group_end("        ")
+        self.shift_cur("        ")
+        e("      }")
+        e("      it_start = 0;")
+        e("      if (c + 1 < a.nc) {")
+        e("        vt::cp_async_wait_all();")
+        e(f"        vt::realign<NL, NWC, {NT}>(curA, llrA, (int)(onA & 15), "
+          "(int)min(max((gA.s - (gA.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
+        e(f"        vt::realign<NL, NWC, {NT}>(curB, llrB, (int)(onB & 15), "
+          "(int)min(max((gB.s - (gB.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
+        e("      }")
+        e("    }")
+        e("    // pending loads of the previous tile's traceback, then its unstored tail")
+        e("    vt::cp_async_wait_all();")
+        e(f"    if (tbA_load) tbA.step(a, (s_tb[tid] >> tb_shA) & {(1 << L) - 1}u);")
+        e(f"    if (tbB_load) tbB.step(a, (s_tb[{NT} + tid] >> tb_shB) & {(1 << L) - 1}u);")
+        e("    while (tbA.running && tbA.b >= a.b_lo) {")
+        e("      uint32_t sh;")
+        e("      const uint32_t w = *field_word(tbA.b, tbA.j, parity_prev, sh);")
+        e(f"      tbA.step(a, (w >> sh) & {(1 << L) - 1}u);")
+        e("    }")
+        e("    while (tbB.running && tbB.b >= a.b_lo) {")
+        e("      uint32_t sh;")
+        e("      const uint32_t w = *field_word(tbB.b, tbB.j, parity_prev, sh);")
+        e(f"      tbB.step(a, (w >> (sh + 16)) & {(1 << L) - 1}u);")
+        e("    }")
+        e("    if (tbA.running) tbA.drain_unstored(a);")
+        e("    if (tbB.running) tbB.drain_unstored(a);")
+        e("    // final states: argmax per window, lowest index on ties (reference.py:138)")
+        e("    uint32_t bestA = 0, bestB = 0;")
+        for j in range(S):
+            e(f"    bestA = max(bestA, ((m{j} & 0xFFFFu) << 8) | {S - 1 - j}u);")
+            e(f"    bestB = max(bestB, ((m{j} >> 16) << 8) | {S - 1 - j}u);")
+        e(f"    const uint32_t jA = {S - 1}u - (bestA & 0xFFu), jB = {S - 1}u - (bestB & 0xFFu);")
+        e("    if (a.final_metric) {")
+        e(f"      const int64_t bias = ((int64_t)a.nc * CH - (int64_t)it0 * {P}) * {self.dmax};")
+        e(f"      if (actA) a.final_metric[wa] = (int64_t)(bestA >> {8 + L}) + offA - bias;")
+        e(f"      if (actB) a.final_metric[wb] = (int64_t)(bestB >> {8 + L}) + offB - bias;")
+        e("    }")
+        e("    tbA.start(gA, jA, actA, ng);")
+        e("    tbB.start(gB, jB, actB, ng);")
+        e("    parity_prev = parity;")
+        e("  }")
+        e("  // traceback of the CTA's last tile")
+        e("  while (tbA.running && tbA.b >= a.b_lo) {")
+        e("    uint32_t sh;")
+        e("    const uint32_t w = *field_word(tbA.b, tbA.j, parity_prev, sh);")
+        e(f"    tbA.step(a, (w >> sh) & {(1 << L) - 1}u);")
+        e("  }")
+        e("  while (tbB.running && tbB.b >= a.b_lo) {")
+        e("    uint32_t sh;")
+        e("    const uint32_t w = *field_word(tbB.b, tbB.j, parity_prev, sh);")
+        e(f"    tbB.step(a, (w >> (sh + 16)) & {(1 << L) - 1}u);")
+        e("  }")
+        e("  if (tbA.running) tbA.drain_unstored(a);")
+        e("  if (tbB.running) tbB.drain_unstored(a);")
+        e("}")
+        e("")
+        return "\n".join(self.lines)

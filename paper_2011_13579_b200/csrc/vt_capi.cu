@@ -33,17 +33,19 @@ struct Geometry {
   int nc, b_lo, nbs;
 };
 
-Geometry geometry(int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1, int BL) {
-  // windows are cut into BL-stage history blocks aligned to the window end
+Geometry geometry(int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1, int CH, int BL) {
+  // windows are cut into CH-stage chunks aligned to the window end; survivor
+  // histories are stored per BL-stage group (BL divides CH)
   Geometry g;
   g.nwin = w1 - w0;
   const int64_t lmax = std::min<int64_t>(N, F + 2 * V);
-  g.nc = (int)((lmax + BL - 1) / BL);
+  g.nc = (int)((lmax + CH - 1) / CH);
+  const int64_t ng = (int64_t)g.nc * (CH / BL);
   const int64_t head = std::min<int64_t>(N, F + V);  // max (stop - emit_start) over windows
-  int64_t blo = ((int64_t)BL * g.nc - head) / BL;     // first block any window needs for its emit range
+  int64_t blo = ((int64_t)CH * g.nc - head) / BL;     // first group any window needs for its emit range
   if (blo < 0) blo = 0;
   g.b_lo = (int)blo;
-  g.nbs = g.nc - g.b_lo;
+  g.nbs = (int)(ng - blo);
   return g;
 }
 
@@ -51,12 +53,13 @@ Geometry geometry(int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1, int B
 // kernel registry: one generated kernel per supported code (gen/registry.inc)
 // ---------------------------------------------------------------------------
 struct KernelEntry {
-  int K, B, T, SL, BL;
+  int K, B, T, WPT, SL, CH, BL, SQ;
   uint32_t gens[VT_MAX_OUTPUTS];
   const void* fn;
 };
 
-#define VT_KERNEL(fn_, K_, B_, T_, SL_, BL_, ...) {K_, B_, T_, SL_, BL_, __VA_ARGS__, (const void*)&fn_},
+#define VT_KERNEL(fn_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, ...) \
+  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, __VA_ARGS__, (const void*)&fn_},
 }  // namespace
 #include "gen/registry_decl.inc"
 namespace {
@@ -69,17 +72,23 @@ const KernelEntry* registry(int* n) {
   return table;
 }
 
+// Kernel variant: "s32" (default) or "16x2" (VT_KERNEL_VARIANT=16x2: two windows per
+// thread in packed 16-bit halves, where a 16x2 kernel exists for the code).
 const KernelEntry* find(const vt_code* c) {
   if (!c) return nullptr;
+  const char* env = getenv("VT_KERNEL_VARIANT");
+  const bool want16 = env && strcmp(env, "16x2") == 0;
   int n;
   const KernelEntry* t = registry(&n);
+  const KernelEntry* best = nullptr;
   for (int i = 0; i < n; ++i) {
     if (t[i].K != c->K || t[i].B != c->B) continue;
     bool same = true;
     for (int b = 0; b < c->B; ++b) same = same && t[i].gens[b] == c->gens[b];
-    if (same) return &t[i];
+    if (!same) continue;
+    if (!best || (want16 ? t[i].WPT > best->WPT : t[i].WPT < best->WPT)) best = &t[i];
   }
-  return nullptr;
+  return best;
 }
 
 int validate(const vt_code* c) {
@@ -106,14 +115,14 @@ int ctas_per_sm(const KernelEntry* k) {
 }
 
 int64_t grid_for(const KernelEntry* k, int64_t nwin) {
-  const int64_t wpc = kNT / k->T;  // windows per CTA
+  const int64_t wpc = (int64_t)kNT * k->WPT / k->T;  // windows per CTA
   const int64_t tiles = (nwin + wpc - 1) / wpc;
   const int64_t cap = (int64_t)device_sms() * ctas_per_sm(k);
   return std::max<int64_t>(1, std::min(tiles, cap));
 }
 
 size_t scratch_bytes(const KernelEntry* k, const Geometry& g, int64_t grid) {
-  return (size_t)grid * g.nbs * std::max(k->SL / 8, 1) * kNT * sizeof(uint4);
+  return (size_t)grid * g.nbs * k->SQ * kNT * sizeof(uint4);
 }
 
 }  // namespace
@@ -129,7 +138,7 @@ int vt_code_supported(const vt_code* code) { return find(code) != nullptr ? 1 : 
 size_t vt_workspace_bytes(const vt_code* code, int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1) {
   const KernelEntry* k = find(code);
   if (!k || N < 1 || F < 1 || V < 0 || w1 <= w0) return 0;
-  const Geometry g = geometry(N, F, V, w0, w1, k->BL);
+  const Geometry g = geometry(N, F, V, w0, w1, k->CH, k->BL);
   return scratch_bytes(k, g, grid_for(k, g.nwin));
 }
 
@@ -158,7 +167,7 @@ int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, 
     return fail(VT_EINVAL, "llr stage range [%lld, %lld) does not cover [%lld, %lld)", (long long)st0,
                 (long long)st1, (long long)need_lo, (long long)need_hi);
 
-  const Geometry g = geometry(N, F, V, w0, w1, k->BL);
+  const Geometry g = geometry(N, F, V, w0, w1, k->CH, k->BL);
   const int64_t grid = grid_for(k, g.nwin);
   const size_t need = scratch_bytes(k, g, grid);
   if (!workspace || workspace_bytes < need)

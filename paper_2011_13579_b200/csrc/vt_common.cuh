@@ -46,6 +46,23 @@ __device__ __forceinline__ int32_t mad_fma(int32_t a, int32_t b, int32_t c) {
   return d;
 }
 
+// packed 16x2 ops (per-half modular add; unsigned max): VIADD.16x2 / VIADDMNMX.U16x2
+__device__ __forceinline__ uint32_t vadd2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t vaddmax2(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("{.reg .b32 t; add.u16x2 t, %1, %2; max.u16x2 %0, t, %3;}" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 // max(a + b, c): ptxas fuses add.s32 + max.s32 into one DPX VIADDMNMX (ALU pipe)
 __device__ __forceinline__ int32_t addmax(int32_t a, int32_t b, int32_t c) {
   int32_t d;

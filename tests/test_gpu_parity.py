@@ -155,3 +155,20 @@ def test_final_metrics_match_oracle(vt):
     bits, metric = vt.decode_batch(llrs.astype(np.float64), spec)
     np.testing.assert_array_equal(bits, want_bits)
     np.testing.assert_array_equal(metric, want_metric.astype(np.float64))
+
+
+@pytest.mark.parametrize("code", ["k7r2", "k7r3"])
+@pytest.mark.parametrize("fv", [(256, 42), (100, 20), (37, 5)])
+def test_packed_16x2_variant_matches_oracle(vt, code, fv, monkeypatch):
+    """The two-windows-per-thread 16x2 kernels (VT_KERNEL_VARIANT=16x2) are bit-exact too."""
+    monkeypatch.setenv("VT_KERNEL_VARIANT", "16x2")
+    k, gens = code_params(CODES, code)
+    spec = vt.CodeSpec(k, gens)
+    f, v = fv
+    _, q = oracle.synthetic_stream(40_000, k, gens, ebn0_db=1.0, seed=11, scale=24.0)
+    want = oracle.decode_stream(q, k, gens, f, v, threads=8)
+    np.testing.assert_array_equal(_device_decode(vt, q, spec, f, v), want)
+    bits, metric = vt.decode_batch(np.transpose(q[:30_000].reshape(60, 500, -1), (0, 2, 1)).astype(float), spec)
+    wb, wm = oracle.decode_batch(np.transpose(q[:30_000].reshape(60, 500, -1), (0, 2, 1)), k, gens)
+    np.testing.assert_array_equal(bits, wb)
+    np.testing.assert_array_equal(metric, wm.astype(np.float64))
