@@ -345,7 +345,7 @@ class Gen:
             e(f"    best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, {1 << d}));")
         e(f"    const uint32_t jst = (uint32_t)({S - 1} - (best & 0xFFFF));")
         e("    if (t == 0 && active && a.final_metric) a.final_metric[wrel] = (int64_t)(best >> 16) + offset;")
-        e("    if (t == 0) tb.start(g, jst, active, a.nc);")
+        e("    if (t == 0) tb.start(g, jst, active, a.nc, a.N);")
         e("    parity_prev = parity;")
         e("  }")
         e("  // traceback of the CTA's last tile (no following tile to hide it behind)")

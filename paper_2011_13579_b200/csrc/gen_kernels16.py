@@ -29,6 +29,7 @@ from __future__ import annotations
 from gen_kernels import NT, parity
 
 CH_BODIES = 2  # loop bodies per LLR chunk
+MINB16 = 1  # CTAs per SM bound (3 forces a 168-register cap: spills + 1.5x scratch footprint measured 25% slower)
 
 
 def history_bits(K: int, B: int) -> int:
@@ -104,17 +105,23 @@ class Gen16:
         self.lines.extend(body)
         return outs
 
-    def group_end(self, ind: str) -> None:
-        """Traceback steps, history fields -> scratch + clear, renormalisation."""
+    def group_end(self, ind: str, ge: int = 0) -> None:
+        """Traceback steps, history fields -> scratch + clear, renormalisation.
+        ge = index of this group end inside the loop body."""
         L, S = self.L, self.S
         e = self.emit
         hm = ((1 << L) - 1) * 0x10001
         lm = (0xFFFF & ~((1 << L) - 1)) * 0x10001
         fm = (1 << L) - 1
-        e(f"{ind}// ---- group end")
-        e(f"{ind}vt::cp_async_wait_all();")
-        e(f"{ind}if (tbA_load) tbA.step(a, (s_tb[tid] >> tb_shA) & {fm}u);")
-        e(f"{ind}if (tbB_load) tbB.step(a, (s_tb[{NT} + tid] >> tb_shB) & {fm}u);")
+        e(f"{ind}// ---- group end: one traceback step per window of the previous tile (fields were")
+        e(f"{ind}// prefetched two groups ahead: the 2^L candidate states of a group are consecutive)")
+        if self.GPB % 2 == 0:  # static buffer alternation: no register copy of an in-flight load
+            p = ge % 2
+            e(f"{ind}tb_step2(tbA, cA{p}, 0);")
+            e(f"{ind}tb_step2(tbB, cB{p}, 16);")
+        else:
+            e(f"{ind}tb_advance(tbA, nxtA, aftA, 0);")
+            e(f"{ind}tb_advance(tbB, nxtB, aftB, 16);")
         e(f"{ind}if (gidx >= a.b_lo) {{")
         e(f"{ind}  const int gs = gidx - a.b_lo;")
         e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {S // 16} * {NT};")
@@ -133,13 +140,6 @@ class Gen16:
             e(f"{ind}  m{j} = vt::mad_u32(h{j}, 0xFFFFFFFFu, m{j});")
         e(f"{ind}}}")
         e(f"{ind}++gidx;")
-        e(f"{ind}tbA_load = tbA.running && tbA.b >= a.b_lo;")
-        e(f"{ind}tbB_load = tbB.running && tbB.b >= a.b_lo;")
-        e(f"{ind}if (tbA_load) vt::cp_async4(&s_tb[tid], field_word(tbA.b, tbA.j, parity_prev, tb_shA));")
-        e(f"{ind}if (tbB_load) {{")
-        e(f"{ind}  vt::cp_async4(&s_tb[{NT} + tid], field_word(tbB.b, tbB.j, parity_prev, tb_shB));")
-        e(f"{ind}  tb_shB += 16;")
-        e(f"{ind}}}")
         e(f"{ind}// renormalise the next group by Lambda_0 - S_b (per window half)")
         e(f"{ind}offA += pendA;")
         e(f"{ind}offB += pendB;")
@@ -173,11 +173,10 @@ class Gen16:
           f"two windows per thread (16x2 halves), {L}-bit history groups, {P}-stage body, {CH}-stage chunks")
         e('#include "../vt_common.cuh"')
         e("")
-        e(f'extern "C" __global__ void __launch_bounds__({NT}, 1) {name}(const vt::StreamArgs a) {{')
+        e(f'extern "C" __global__ void __launch_bounds__({NT}, {MINB16}) {name}(const vt::StreamArgs a) {{')
         e(f"  constexpr int B = {B}, K = {K}, CH = {CH}, NL = {NL}, NWC = {NWC};")
         e("  const int tid = threadIdx.x;")
         e(f"  __shared__ __align__(16) uint4 s_llr[2 * NL * {NT}];")
-        e(f"  __shared__ uint32_t s_tb[2 * {NT}];")
         e("  const uint64_t pol_last = vt::policy_evict_last();")
         e("  const int64_t nwin = a.w1 - a.w0;")
         e("  const int64_t buf_bytes = (a.st1 - a.st0) * B;")
@@ -188,12 +187,35 @@ class Gen16:
         e("  tbA.running = tbB.running = false;")
         e("  tbA.active = tbB.active = false;")
         e("  int parity_prev = 0, parity = 0;")
-        e("  auto field_word = [&](int grp, uint32_t j, int par, uint32_t& sh) -> const uint32_t* {")
+        e("  uint2 nxtA = make_uint2(0u, 0u), aftA = nxtA, nxtB = nxtA, aftB = nxtA;")
+        e("  uint2 cA0 = nxtA, cA1 = nxtA, cB0 = nxtA, cB1 = nxtA;  // two-deep prefetch buffers (static roles)")
+        e("  // history words of group grp: 4 states per 32-bit word (L bits each, +16 for window B);")
+        e("  // cand(grp, base): the 8-byte word pair holding states base..base+7 (base % 8 == 0)")
+        e("  auto cand = [&](int grp, uint32_t base, int par) -> uint2 {")
         e("    const int gs = grp - a.b_lo;")
         e("    const int x = par ? (a.nbs - 1 - gs) : gs;")
-        e(f"    sh = {L} * (j & 3);")
-        e(f"    const uint4* q = slot + ((size_t)x * {SQ} + (j >> 4)) * {NT};")
-        e("    return reinterpret_cast<const uint32_t*>(q) + ((j >> 2) & 3);")
+        e(f"    const uint4* q = slot + ((size_t)x * {SQ} + (base >> 4)) * {NT};")
+        e("    return __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint32_t*>(q) + ((base >> 2) & 2)));")
+        e("  };")
+        e(f"  auto tb_advance = [&](vt::Traceback<K, {L}>& tb, uint2& nxt, uint2& aft, int side) {{")
+        e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
+        e("    const uint32_t li = tb.j & 7u;")
+        e("    const uint32_t w = (li & 4u) ? nxt.y : nxt.x;")
+        e(f"    tb.step(a, (w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
+        e("    nxt = aft;")
+        e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u, parity_prev);")
+        e("  };")
+        e(f"  auto tb_step2 = [&](vt::Traceback<K, {L}>& tb, uint2& buf, int side) {{")
+        e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
+        e("    const uint32_t li = tb.j & 7u;")
+        e("    const uint32_t w = (li & 4u) ? buf.y : buf.x;")
+        e(f"    tb.step(a, (w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
+        e(f"    if (tb.b - 1 >= a.b_lo) buf = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u, parity_prev);")
+        e("  };")
+        e(f"  auto tb_begin = [&](vt::Traceback<K, {L}>& tb, uint2& nxt, uint2& aft) {{")
+        e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
+        e("    nxt = cand(tb.b, tb.j & ~7u, parity);")
+        e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u, parity);")
         e("  };")
         e(f"  const int ng = a.nc * {CH // L};  // history groups per window")
         e(f"  for (int64_t tile = blockIdx.x; tile * {2 * NT} < nwin; tile += gridDim.x, parity ^= 1) {{")
@@ -220,14 +242,6 @@ class Gen16:
           f"(int)min(max((gB.s - gB.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
         e(f"    int gidx = it0 * {self.GPB};")
         e("    // traceback of the previous tile: one group step per forward group, loads one group ahead")
-        e("    uint32_t tb_shA = 0, tb_shB = 0;")
-        e("    bool tbA_load = tbA.running && tbA.b >= a.b_lo;")
-        e("    bool tbB_load = tbB.running && tbB.b >= a.b_lo;")
-        e("    if (tbA_load) vt::cp_async4(&s_tb[tid], field_word(tbA.b, tbA.j, parity_prev, tb_shA));")
-        e("    if (tbB_load) {")
-        e(f"      vt::cp_async4(&s_tb[{NT} + tid], field_word(tbB.b, tbB.j, parity_prev, tb_shB));")
-        e("      tb_shB += 16;")
-        e("    }")
         e("    for (int c = 0; c < a.nc; ++c) {")
         e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
         e("      if (c + 1 < a.nc) {")
@@ -246,7 +260,7 @@ class Gen16:
                 for j in range(S):
                     e(f"        m{j} = {names[j]};")
                 names = [f"m{j}" for j in range(S)]
-                self.group_end("        ")
+                self.group_end("        ", q // L)
         self.shift_cur("        ")
         e("      }")
         e("      it_start = 0;")
@@ -258,20 +272,13 @@ class Gen16:
           "(int)min(max((gB.s - (gB.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
         e("      }")
         e("    }")
-        e("    // pending loads of the previous tile's traceback, then its unstored tail")
-        e("    vt::cp_async_wait_all();")
-        e(f"    if (tbA_load) tbA.step(a, (s_tb[tid] >> tb_shA) & {(1 << L) - 1}u);")
-        e(f"    if (tbB_load) tbB.step(a, (s_tb[{NT} + tid] >> tb_shB) & {(1 << L) - 1}u);")
-        e("    while (tbA.running && tbA.b >= a.b_lo) {")
-        e("      uint32_t sh;")
-        e("      const uint32_t w = *field_word(tbA.b, tbA.j, parity_prev, sh);")
-        e(f"      tbA.step(a, (w >> sh) & {(1 << L) - 1}u);")
-        e("    }")
-        e("    while (tbB.running && tbB.b >= a.b_lo) {")
-        e("      uint32_t sh;")
-        e("      const uint32_t w = *field_word(tbB.b, tbB.j, parity_prev, sh);")
-        e(f"      tbB.step(a, (w >> (sh + 16)) & {(1 << L) - 1}u);")
-        e("    }")
+        e("    // the previous tile's remaining traceback steps, then its unstored tail")
+        if self.GPB % 2 == 0:
+            e("    while (tbA.running && tbA.b >= a.b_lo) { tb_step2(tbA, cA0, 0); tb_step2(tbA, cA1, 0); }")
+            e("    while (tbB.running && tbB.b >= a.b_lo) { tb_step2(tbB, cB0, 16); tb_step2(tbB, cB1, 16); }")
+        else:
+            e("    while (tbA.running && tbA.b >= a.b_lo) tb_advance(tbA, nxtA, aftA, 0);")
+            e("    while (tbB.running && tbB.b >= a.b_lo) tb_advance(tbB, nxtB, aftB, 16);")
         e("    if (tbA.running) tbA.drain_unstored(a);")
         e("    if (tbB.running) tbB.drain_unstored(a);")
         e("    // final states: argmax per window, lowest index on ties (reference.py:138)")
@@ -285,21 +292,23 @@ class Gen16:
         e(f"      if (actA) a.final_metric[wa] = (int64_t)(bestA >> {8 + L}) + offA - bias;")
         e(f"      if (actB) a.final_metric[wb] = (int64_t)(bestB >> {8 + L}) + offB - bias;")
         e("    }")
-        e("    tbA.start(gA, jA, actA, ng);")
-        e("    tbB.start(gB, jB, actB, ng);")
+        e("    tbA.start(gA, jA, actA, ng, a.N);")
+        e("    tbB.start(gB, jB, actB, ng, a.N);")
+        if self.GPB % 2 == 0:
+            e("    tb_begin(tbA, cA0, cA1);")
+            e("    tb_begin(tbB, cB0, cB1);")
+        else:
+            e("    tb_begin(tbA, nxtA, aftA);")
+            e("    tb_begin(tbB, nxtB, aftB);")
         e("    parity_prev = parity;")
         e("  }")
         e("  // traceback of the CTA's last tile")
-        e("  while (tbA.running && tbA.b >= a.b_lo) {")
-        e("    uint32_t sh;")
-        e("    const uint32_t w = *field_word(tbA.b, tbA.j, parity_prev, sh);")
-        e(f"    tbA.step(a, (w >> sh) & {(1 << L) - 1}u);")
-        e("  }")
-        e("  while (tbB.running && tbB.b >= a.b_lo) {")
-        e("    uint32_t sh;")
-        e("    const uint32_t w = *field_word(tbB.b, tbB.j, parity_prev, sh);")
-        e(f"    tbB.step(a, (w >> (sh + 16)) & {(1 << L) - 1}u);")
-        e("  }")
+        if self.GPB % 2 == 0:
+            e("  while (tbA.running && tbA.b >= a.b_lo) { tb_step2(tbA, cA0, 0); tb_step2(tbA, cA1, 0); }")
+            e("  while (tbB.running && tbB.b >= a.b_lo) { tb_step2(tbB, cB0, 16); tb_step2(tbB, cB1, 16); }")
+        else:
+            e("  while (tbA.running && tbA.b >= a.b_lo) tb_advance(tbA, nxtA, aftA, 0);")
+            e("  while (tbB.running && tbB.b >= a.b_lo) tb_advance(tbB, nxtB, aftB, 16);")
         e("  if (tbA.running) tbA.drain_unstored(a);")
         e("  if (tbB.running) tbB.drain_unstored(a);")
         e("}")

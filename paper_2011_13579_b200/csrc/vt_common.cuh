@@ -182,64 +182,73 @@ __device__ __forceinline__ int32_t llr_hi16(uint32_t word, uint32_t sh) {
 template <int K, int BL>
 struct Traceback {
   static constexpr uint32_t S = 1u << (K - 1);
-  int64_t e0, e1, g0, top, hiw, loww, lo;
+  // positions are relative to P0 = floor32(e0), so all bookkeeping is 32-bit
+  int64_t wbase;   // absolute word index of relative word 0
+  int e0r, e1r;    // relative emit range
+  int nr;          // stream end (N) relative, clamped to 2^30
+  int top;         // relative word-aligned top of the emitted words
+  int gb;          // relative position of block b's first stage
+  int hiw;         // next (relative) word to flush; done when < 0
+  int lo;          // acc holds decoded bits of relative positions [lo, (hiw+1)*32)
   uint64_t acc;
   uint32_t j;
-  int b;         // next block (descending)
-  bool active;   // emits output (window exists)
-  bool running;  // words left to emit
+  int b;           // next block (descending)
+  bool active;     // emits output (window exists)
+  bool running;    // words left to emit
 
-  __device__ __forceinline__ void start(const Window& g, uint32_t jst, bool act, int nc) {
-    e0 = g.e0;
-    e1 = g.e1;
-    g0 = g.g0;
-    top = ((g.e1 + 31) >> 5) << 5;
-    hiw = (g.e1 - 1) >> 5;
-    loww = g.e0 >> 5;
+  __device__ __forceinline__ void start(const Window& g, uint32_t jst, bool act, int nblocks, int64_t N) {
+    const int64_t p0 = (g.e0 >> 5) << 5;
+    wbase = g.e0 >> 5;
+    e0r = (int)(g.e0 - p0);
+    e1r = (int)(g.e1 - p0);
+    nr = (int)min(N - p0, (int64_t)(1 << 30));
+    top = ((e1r + 31) >> 5) << 5;
+    hiw = (e1r - 1) >> 5;
+    gb = (int)(g.g0 - p0) + BL * (nblocks - 1);
     lo = top;
     acc = 0;
     j = jst;
-    b = nc - 1;
+    b = nblocks - 1;
     active = act;
-    running = hiw >= loww;
+    running = true;
   }
 
   __device__ __forceinline__ void flush(const StreamArgs& a) {
-    const int64_t wlo = hiw << 5, whi = wlo + 32;
+    const int wlo = hiw << 5, whi = wlo + 32;
     uint32_t word = (uint32_t)(wlo >= lo ? (acc >> (wlo - lo)) : (acc << (lo - wlo)));
-    const int64_t vlo = max(wlo, e0), vhi = min(whi, e1);
+    const int vlo = max(wlo, e0r), vhi = min(whi, e1r);
     const uint32_t mask = (vhi - vlo >= 32) ? 0xFFFFFFFFu : (((1u << (vhi - vlo)) - 1u) << (vlo - wlo));
     word &= mask;
     if (active) {
-      const bool owned = (wlo >= e0) && (min(whi, a.N) <= e1);
-      if (owned) a.bits[hiw] = word;
-      else if (word) atomicOr(a.bits + hiw, word);
+      const bool owned = (wlo >= e0r) && (min(whi, nr) <= e1r);
+      if (owned) a.bits[wbase + hiw] = word;
+      else if (word) atomicOr(a.bits + wbase + hiw, word);
     }
     --hiw;
-    const int64_t keep = ((hiw + 1) << 5) - lo;
+    const int keep = ((hiw + 1) << 5) - lo;
     acc &= (keep >= 64) ? ~0ull : (keep > 0 ? ((1ull << keep) - 1ull) : 0ull);
+    running = hiw >= 0;
   }
 
   // consume block b with history h (0 for blocks that were not stored)
   __device__ __forceinline__ void step(const StreamArgs& a, uint32_t h) {
-    const int64_t gb = g0 + BL * (int64_t)b;
-    uint32_t bits = (uint32_t)(((uint64_t)h | ((uint64_t)j << BL)) >> (K - 1)) & ((1u << BL) - 1u);
-    j = (uint32_t)(((uint64_t)j << BL) | h) & (S - 1);
+    uint32_t bits = ((h | (j << BL)) >> (K - 1)) & ((1u << BL) - 1u);
+    j = ((j << BL) | h) & (S - 1);
+    const int p = gb;
+    gb -= BL;
     --b;
-    if (gb >= top) return;
-    const int n_new = (int)(lo - gb);  // BL, or less for the block straddling `top`
+    if (p >= top) return;
+    const int n_new = lo - p;  // BL, or more/less for the block straddling `top`
     if (n_new < BL) bits &= (1u << n_new) - 1u;
     acc = (acc << n_new) | bits;
-    lo = gb;
-    while (hiw >= loww && (hiw << 5) >= lo) flush(a);
-    running = hiw >= loww;
+    lo = p;
+    while (running && (hiw << 5) >= lo) flush(a);
   }
 
   // blocks below the stored range and words starting before the first chunk
   __device__ __forceinline__ void drain_unstored(const StreamArgs& a) {
     while (running && b >= 0) step(a, 0u);
-    while (hiw >= loww) flush(a);
-    running = false;
+    while (running) flush(a);
   }
 };
 
