@@ -106,15 +106,26 @@ class Gen16:
         return outs
 
     def group_end(self, ind: str, ge: int = 0) -> None:
-        """Traceback steps, history fields -> scratch + clear, renormalisation.
+        """Renormalisation, traceback steps, history fields -> scratch + clear.
         ge = index of this group end inside the loop body."""
         L, S = self.L, self.S
         e = self.emit
         hm = ((1 << L) - 1) * 0x10001
         lm = (0xFFFF & ~((1 << L) - 1)) * 0x10001
-        fm = (1 << L) - 1
-        e(f"{ind}// ---- group end: one traceback step per window of the previous tile (fields were")
-        e(f"{ind}// prefetched two groups ahead: the 2^L candidate states of a group are consecutive)")
+        e(f"{ind}// ---- group end")
+        e(f"{ind}// renormalise the next group by Lambda_0 - S_b (per window half); from the fresh")
+        e(f"{ind}// state-0 metric (history masked), so the chain overlaps the rest of the group end")
+        e(f"{ind}offA += pendA;")
+        e(f"{ind}offB += pendB;")
+        e(f"{ind}{{")
+        e(f"{ind}  const uint32_t r0 = m0 & {lm:#x}u;")
+        e(f"{ind}  const uint32_t rr = vt::vadd2(r0, {((-(self.Sb << L)) & 0xFFFF) * 0x10001:#x}u);")
+        e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);")
+        e(f"{ind}  pendA = (int64_t)((r0 & 0xFFFFu) >> {L}) - {self.Sb};")
+        e(f"{ind}  pendB = (int64_t)(r0 >> {16 + L}) - {self.Sb};")
+        e(f"{ind}}}")
+        e(f"{ind}// one traceback step per window of the previous tile (fields prefetched two groups")
+        e(f"{ind}// ahead: the 2^L candidate states of a group are consecutive)")
         if self.GPB % 2 == 0:  # static buffer alternation: no register copy of an in-flight load
             p = ge % 2
             e(f"{ind}tb_step2(tbA, cA{p}, 0);")
@@ -140,16 +151,6 @@ class Gen16:
             e(f"{ind}  m{j} = vt::mad_u32(h{j}, 0xFFFFFFFFu, m{j});")
         e(f"{ind}}}")
         e(f"{ind}++gidx;")
-        e(f"{ind}// renormalise the next group by Lambda_0 - S_b (per window half)")
-        e(f"{ind}offA += pendA;")
-        e(f"{ind}offB += pendB;")
-        e(f"{ind}{{")
-        e(f"{ind}  const uint32_t r0 = m0 & {lm:#x}u;")
-        e(f"{ind}  const uint32_t rr = vt::vadd2(r0, {((-(self.Sb << L)) & 0xFFFF) * 0x10001:#x}u);")
-        e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);")
-        e(f"{ind}  pendA = (int64_t)((r0 & 0xFFFFu) >> {L}) - {self.Sb};")
-        e(f"{ind}  pendB = (int64_t)(r0 >> {16 + L}) - {self.Sb};")
-        e(f"{ind}}}")
 
     def shift_cur(self, ind: str) -> None:
         nb = self.P * self.B
@@ -183,7 +184,7 @@ class Gen16:
         e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {SQ} * {NT} + tid;")
         e("  uint4* const llrA = s_llr + tid;")
         e(f"  uint4* const llrB = s_llr + NL * {NT} + tid;")
-        e(f"  vt::Traceback<K, {L}> tbA, tbB;")
+        e(f"  vt::TracebackLite<K, {L}> tbA, tbB;")
         e("  tbA.running = tbB.running = false;")
         e("  tbA.active = tbB.active = false;")
         e("  int parity_prev = 0, parity = 0;")
@@ -197,22 +198,23 @@ class Gen16:
         e(f"    const uint4* q = slot + ((size_t)x * {SQ} + (base >> 4)) * {NT};")
         e("    return __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint32_t*>(q) + ((base >> 2) & 2)));")
         e("  };")
-        e(f"  auto tb_advance = [&](vt::Traceback<K, {L}>& tb, uint2& nxt, uint2& aft, int side) {{")
+        e(f"  auto tb_advance = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft, int side) {{")
         e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
         e("    const uint32_t li = tb.j & 7u;")
         e("    const uint32_t w = (li & 4u) ? nxt.y : nxt.x;")
-        e(f"    tb.step(a, (w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
+        e(f"    tb.step((w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
+        e("    tb.settle(a);")
         e("    nxt = aft;")
         e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u, parity_prev);")
         e("  };")
-        e(f"  auto tb_step2 = [&](vt::Traceback<K, {L}>& tb, uint2& buf, int side) {{")
+        e(f"  auto tb_step2 = [&](vt::TracebackLite<K, {L}>& tb, uint2& buf, int side) {{")
         e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
         e("    const uint32_t li = tb.j & 7u;")
         e("    const uint32_t w = (li & 4u) ? buf.y : buf.x;")
-        e(f"    tb.step(a, (w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
+        e(f"    tb.step((w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
         e(f"    if (tb.b - 1 >= a.b_lo) buf = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u, parity_prev);")
         e("  };")
-        e(f"  auto tb_begin = [&](vt::Traceback<K, {L}>& tb, uint2& nxt, uint2& aft) {{")
+        e(f"  auto tb_begin = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft) {{")
         e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
         e("    nxt = cand(tb.b, tb.j & ~7u, parity);")
         e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u, parity);")
@@ -264,6 +266,8 @@ class Gen16:
         self.shift_cur("        ")
         e("      }")
         e("      it_start = 0;")
+        e("      tbA.settle(a);  // whole words of the previous tile's traceback")
+        e("      tbB.settle(a);")
         e("      if (c + 1 < a.nc) {")
         e("        vt::cp_async_wait_all();")
         e(f"        vt::realign<NL, NWC, {NT}>(curA, llrA, (int)(onA & 15), "
@@ -274,8 +278,8 @@ class Gen16:
         e("    }")
         e("    // the previous tile's remaining traceback steps, then its unstored tail")
         if self.GPB % 2 == 0:
-            e("    while (tbA.running && tbA.b >= a.b_lo) { tb_step2(tbA, cA0, 0); tb_step2(tbA, cA1, 0); }")
-            e("    while (tbB.running && tbB.b >= a.b_lo) { tb_step2(tbB, cB0, 16); tb_step2(tbB, cB1, 16); }")
+            e("    while (tbA.running && tbA.b >= a.b_lo) { tb_step2(tbA, cA0, 0); tb_step2(tbA, cA1, 0); tbA.settle(a); }")
+            e("    while (tbB.running && tbB.b >= a.b_lo) { tb_step2(tbB, cB0, 16); tb_step2(tbB, cB1, 16); tbB.settle(a); }")
         else:
             e("    while (tbA.running && tbA.b >= a.b_lo) tb_advance(tbA, nxtA, aftA, 0);")
             e("    while (tbB.running && tbB.b >= a.b_lo) tb_advance(tbB, nxtB, aftB, 16);")
@@ -304,8 +308,8 @@ class Gen16:
         e("  }")
         e("  // traceback of the CTA's last tile")
         if self.GPB % 2 == 0:
-            e("  while (tbA.running && tbA.b >= a.b_lo) { tb_step2(tbA, cA0, 0); tb_step2(tbA, cA1, 0); }")
-            e("  while (tbB.running && tbB.b >= a.b_lo) { tb_step2(tbB, cB0, 16); tb_step2(tbB, cB1, 16); }")
+            e("  while (tbA.running && tbA.b >= a.b_lo) { tb_step2(tbA, cA0, 0); tb_step2(tbA, cA1, 0); tbA.settle(a); }")
+            e("  while (tbB.running && tbB.b >= a.b_lo) { tb_step2(tbB, cB0, 16); tb_step2(tbB, cB1, 16); tbB.settle(a); }")
         else:
             e("  while (tbA.running && tbA.b >= a.b_lo) tb_advance(tbA, nxtA, aftA, 0);")
             e("  while (tbB.running && tbB.b >= a.b_lo) tb_advance(tbB, nxtB, aftB, 16);")

@@ -252,4 +252,74 @@ struct Traceback {
   }
 };
 
+// Branch-free traceback step for short history groups (L < K-1 bits per group,
+// the 16x2 kernels): each step shifts L decoded bits into a 64-bit register;
+// whole words are written by settle(), called once per chunk (<= 43 pending
+// bits, so nothing shifts out before it is written).
+template <int K, int L>
+struct TracebackLite {
+  static constexpr uint32_t S = 1u << (K - 1);
+  int64_t wbase;   // absolute word index of relative word 0 (P0 = floor32(e0))
+  int e0r, e1r, nr;
+  int hiw;         // next relative word to write; finished when < 0
+  int lo;          // relative position of bit 0 of acc
+  uint64_t acc;
+  uint32_t j;
+  int b;           // next group (descending)
+  bool active, running;
+
+  __device__ __forceinline__ void start(const Window& g, uint32_t jst, bool act, int ngroups, int64_t N) {
+    const int64_t p0 = (g.e0 >> 5) << 5;
+    wbase = g.e0 >> 5;
+    e0r = (int)(g.e0 - p0);
+    e1r = (int)(g.e1 - p0);
+    nr = (int)min(N - p0, (int64_t)(1 << 30));
+    hiw = (e1r - 1) >> 5;
+    lo = (int)(g.g0 - p0) + L * ngroups;  // window end: nothing accumulated yet
+    acc = 0;
+    j = jst;
+    b = ngroups - 1;
+    active = act;
+    running = true;
+  }
+  // consume the history h of group b for the current state j
+  __device__ __forceinline__ void step(uint32_t h) {
+    const uint32_t bits = (j >> (K - 1 - L)) & ((1u << L) - 1u);  // inputs of the group's stages
+    j = ((j << L) | h) & (S - 1);
+    acc = (acc << L) | bits;
+    lo -= L;
+    --b;
+  }
+  __device__ __forceinline__ void settle(const StreamArgs& a) {
+    while (running && (hiw << 5) >= lo) {
+      const int wlo = hiw << 5, whi = wlo + 32;
+      uint32_t word = (uint32_t)(acc >> (wlo - lo));
+      const int vlo = max(wlo, e0r), vhi = min(whi, e1r);
+      word &= (vhi - vlo >= 32) ? 0xFFFFFFFFu : (((1u << (vhi - vlo)) - 1u) << (vlo - wlo));
+      if (active) {
+        if ((wlo >= e0r) && (min(whi, nr) <= e1r)) a.bits[wbase + hiw] = word;
+        else if (word) atomicOr(a.bits + wbase + hiw, word);
+      }
+      --hiw;
+      running = hiw >= 0;
+    }
+  }
+  // groups below the stored range (their decisions are never emitted)
+  __device__ __forceinline__ void drain_unstored(const StreamArgs& a) {
+    while (running && b >= 0) {
+      step(0u);
+      settle(a);
+    }
+    if (running) {  // words starting before the window's first group
+      while (running) {
+        const int wlo = hiw << 5;
+        const int sh = lo - wlo;  // > 0: bits below lo are outside the window
+        lo = wlo;
+        acc = sh < 64 ? acc << sh : 0ull;
+        settle(a);
+      }
+    }
+  }
+};
+
 }  // namespace vt
