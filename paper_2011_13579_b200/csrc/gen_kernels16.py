@@ -70,7 +70,15 @@ class Gen16:
         self.lines.append(s)
 
     def stage(self, ind: str, q: int, names: list[str]) -> list[str]:
-        """One radix-2 stage (body position q) for both windows."""
+        """One radix-2 stage (body position q) for both windows.
+
+        Candidate i1 is formed with a plain 32-bit IMAD (FMA pipe): every per-half
+        value stays inside [0, 2^16) (range argument in the module docstring), so a
+        32-bit add of the integer-packed addend E32 = e_B * 2^16 + e_A is exact per
+        half even when e_A < 0 (renormalisation stage).  Candidate i0 goes through
+        the fused VIADDMNMX.U16x2 add, which wraps per half, so it takes the
+        per-half (mod 2^16) form D16.  Off the renormalisation stage the two forms
+        coincide (all halves >= 0)."""
         B, L, S = self.B, self.L, self.S
         gq = q % L
         flag = f"cflag{q - gq}"
@@ -93,15 +101,19 @@ class Gen16:
             need_e.add(p1)
             nm = f"x{q}_{j}"
             body.append(f"{ind}const uint32_t {nm} = vt::vaddmax2({names[i0]}, D{q}_{p0}, "
-                        f"vt::vadd2({names[i1]}, E{q}_{p1}));")
+                        f"vt::mad_u32({names[i1]}, 1u, E{q}_{p1}));")
             outs.append(nm)
+        if gq == 0:
+            e(f"{ind}const uint32_t kE{q} = negE + {flag} * 0x10001u;")
         for p in sorted(need_d | need_e):
             expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(B))
-            if gq == 0:
-                expr = f"vt::vadd2({expr}, negR)"
-            e(f"{ind}const uint32_t D{q}_{p} = {expr};")
+            e(f"{ind}const uint32_t S{q}_{p} = {expr};")
+            if p in need_d:
+                d = f"vt::vadd2(S{q}_{p}, negR)" if gq == 0 else f"S{q}_{p}"
+                e(f"{ind}const uint32_t D{q}_{p} = {d};")
             if p in need_e:
-                e(f"{ind}const uint32_t E{q}_{p} = vt::vadd2(D{q}_{p}, {flag} * {(1 << gq) * 0x10001:#x}u);")
+                k = f"kE{q}" if gq == 0 else f"{flag} * {(1 << gq) * 0x10001:#x}u"
+                e(f"{ind}const uint32_t E{q}_{p} = S{q}_{p} + {k};")
         self.lines.extend(body)
         return outs
 
@@ -120,7 +132,8 @@ class Gen16:
         e(f"{ind}{{")
         e(f"{ind}  const uint32_t r0 = m0 & {lm:#x}u;")
         e(f"{ind}  const uint32_t rr = vt::vadd2(r0, {((-(self.Sb << L)) & 0xFFFF) * 0x10001:#x}u);")
-        e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);")
+        e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);  // -R per half, mod 2^16 (fused-add operand)")
+        e(f"{ind}  negE = {(self.Sb << L) * 0x10001:#x}u - r0;  // -R as a packed integer (IMAD operand)")
         e(f"{ind}  pendA = (int64_t)((r0 & 0xFFFFu) >> {L}) - {self.Sb};")
         e(f"{ind}  pendB = (int64_t)(r0 >> {16 + L}) - {self.Sb};")
         e(f"{ind}}}")
@@ -177,13 +190,14 @@ class Gen16:
         e(f'extern "C" __global__ void __launch_bounds__({NT}, {MINB16}) {name}(const vt::StreamArgs a) {{')
         e(f"  constexpr int B = {B}, K = {K}, CH = {CH}, NL = {NL}, NWC = {NWC};")
         e("  const int tid = threadIdx.x;")
-        e(f"  __shared__ __align__(16) uint4 s_llr[2 * NL * {NT}];")
+        e(f"  // LLR staging: 2 buffers (chunk parity) x 2 windows x NL uint4 per thread (column layout)")
+        e(f"  __shared__ __align__(16) uint4 s_llr[4 * NL * {NT}];")
         e("  const uint64_t pol_last = vt::policy_evict_last();")
         e("  const int64_t nwin = a.w1 - a.w0;")
         e("  const int64_t buf_bytes = (a.st1 - a.st0) * B;")
         e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {SQ} * {NT} + tid;")
-        e("  uint4* const llrA = s_llr + tid;")
-        e(f"  uint4* const llrB = s_llr + NL * {NT} + tid;")
+        e(f"  auto llrA = [&](int buf) {{ return s_llr + (2 * buf) * NL * {NT} + tid; }};")
+        e(f"  auto llrB = [&](int buf) {{ return s_llr + (2 * buf + 1) * NL * {NT} + tid; }};")
         e(f"  vt::TracebackLite<K, {L}> tbA, tbB;")
         e("  tbA.running = tbB.running = false;")
         e("  tbA.active = tbB.active = false;")
@@ -192,11 +206,11 @@ class Gen16:
         e("  uint2 cA0 = nxtA, cA1 = nxtA, cB0 = nxtA, cB1 = nxtA;  // two-deep prefetch buffers (static roles)")
         e("  // history words of group grp: 4 states per 32-bit word (L bits each, +16 for window B);")
         e("  // cand(grp, base): the 8-byte word pair holding states base..base+7 (base % 8 == 0)")
-        e("  auto cand = [&](int grp, uint32_t base, int par) -> uint2 {")
-        e("    const int gs = grp - a.b_lo;")
-        e("    const int x = par ? (a.nbs - 1 - gs) : gs;")
-        e(f"    const uint4* q = slot + ((size_t)x * {SQ} + (base >> 4)) * {NT};")
-        e("    return __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint32_t*>(q) + ((base >> 2) & 2)));")
+        e("  // traced tile: group grp sits at slot position x = txa + txs * grp (tiles alternate the order)")
+        e("  int txa = 0, txs = 1;")
+        e("  auto cand = [&](int grp, uint32_t base) -> uint2 {")
+        e(f"    const uint32_t off = (uint32_t)(txa + txs * grp) * {SQ * NT * 16}u + (base >> 4) * {NT * 16}u + (base & 8u);")
+        e("    return __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(slot) + off));")
         e("  };")
         e(f"  auto tb_advance = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft, int side) {{")
         e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
@@ -205,19 +219,19 @@ class Gen16:
         e(f"    tb.step((w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
         e("    tb.settle(a);")
         e("    nxt = aft;")
-        e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u, parity_prev);")
+        e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
         e("  };")
         e(f"  auto tb_step2 = [&](vt::TracebackLite<K, {L}>& tb, uint2& buf, int side) {{")
         e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
         e("    const uint32_t li = tb.j & 7u;")
         e("    const uint32_t w = (li & 4u) ? buf.y : buf.x;")
         e(f"    tb.step((w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
-        e(f"    if (tb.b - 1 >= a.b_lo) buf = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u, parity_prev);")
+        e(f"    if (tb.b - 1 >= a.b_lo) buf = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
         e("  };")
         e(f"  auto tb_begin = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft) {{")
         e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
-        e("    nxt = cand(tb.b, tb.j & ~7u, parity);")
-        e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u, parity);")
+        e("    nxt = cand(tb.b, tb.j & ~7u);")
+        e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
         e("  };")
         e(f"  const int ng = a.nc * {CH // L};  // history groups per window")
         e(f"  for (int64_t tile = blockIdx.x; tile * {2 * NT} < nwin; tile += gridDim.x, parity ^= 1) {{")
@@ -227,7 +241,7 @@ class Gen16:
         e(f"    const vt::Window gB = vt::window_geometry<{CH}>(a, a.w0 + (actB ? wb : nwin - 1));")
         e("    const int64_t oA = (gA.g0 - a.st0) * B, oB = (gB.g0 - a.st0) * B;")
         e("    " + " ".join(f"uint32_t m{j} = 0;" for j in range(S)))
-        e("    uint32_t negR = 0;")
+        e("    uint32_t negR = 0, negE = 0;")
         e("    int64_t offA = 0, offB = 0, pendA = 0, pendB = 0;")
         e("    uint32_t curA[NWC], curB[NWC];")
         e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole bodies of it")
@@ -235,21 +249,29 @@ class Gen16:
           f"(int64_t){CH_BODIES});")
         e("    int it_start = it0;")
         e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
-        e(f"    vt::stage_llr<NL, {NT}>(llrA, a.llr, buf_bytes, oA0, 0);")
-        e(f"    vt::stage_llr<NL, {NT}>(llrB, a.llr, buf_bytes, oB0, 0);")
-        e("    vt::cp_async_wait_all();")
-        e(f"    vt::realign<NL, NWC, {NT}>(curA, llrA, (int)(oA0 & 15), "
+        e("    // chunks are staged two ahead (cp.async groups): chunk k lives in buffer k & 1")
+        e(f"    vt::stage_llr<NL, {NT}>(llrA(0), a.llr, buf_bytes, oA0, 0);")
+        e(f"    vt::stage_llr<NL, {NT}>(llrB(0), a.llr, buf_bytes, oB0, 0);")
+        e("    vt::cp_async_commit();")
+        e("    if (a.nc > 1) {")
+        e(f"      vt::stage_llr<NL, {NT}>(llrA(1), a.llr, buf_bytes, oA + (int64_t)CH * B, 0);")
+        e(f"      vt::stage_llr<NL, {NT}>(llrB(1), a.llr, buf_bytes, oB + (int64_t)CH * B, 0);")
+        e("    }")
+        e("    vt::cp_async_commit();")
+        e("    vt::cp_async_wait_group<1>();")
+        e(f"    vt::realign<NL, NWC, {NT}>(curA, llrA(0), (int)(oA0 & 15), "
           f"(int)min(max((gA.s - gA.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
-        e(f"    vt::realign<NL, NWC, {NT}>(curB, llrB, (int)(oB0 & 15), "
+        e(f"    vt::realign<NL, NWC, {NT}>(curB, llrB(0), (int)(oB0 & 15), "
           f"(int)min(max((gB.s - gB.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
         e(f"    int gidx = it0 * {self.GPB};")
         e("    // traceback of the previous tile: one group step per forward group, loads one group ahead")
         e("    for (int c = 0; c < a.nc; ++c) {")
         e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
-        e("      if (c + 1 < a.nc) {")
-        e(f"        vt::stage_llr<NL, {NT}>(llrA, a.llr, buf_bytes, onA, 0);")
-        e(f"        vt::stage_llr<NL, {NT}>(llrB, a.llr, buf_bytes, onB, 0);")
+        e("      if (c + 2 < a.nc) {")
+        e(f"        vt::stage_llr<NL, {NT}>(llrA(c & 1), a.llr, buf_bytes, onA + (int64_t)CH * B, 0);")
+        e(f"        vt::stage_llr<NL, {NT}>(llrB(c & 1), a.llr, buf_bytes, onB + (int64_t)CH * B, 0);")
         e("      }")
+        e("      vt::cp_async_commit();")
         e("#pragma unroll 1")
         e(f"      for (int it = it_start; it < {CH_BODIES}; ++it) {{")
         names = [f"m{j}" for j in range(S)]
@@ -269,10 +291,10 @@ class Gen16:
         e("      tbA.settle(a);  // whole words of the previous tile's traceback")
         e("      tbB.settle(a);")
         e("      if (c + 1 < a.nc) {")
-        e("        vt::cp_async_wait_all();")
-        e(f"        vt::realign<NL, NWC, {NT}>(curA, llrA, (int)(onA & 15), "
+        e("        vt::cp_async_wait_group<1>();")
+        e(f"        vt::realign<NL, NWC, {NT}>(curA, llrA((c + 1) & 1), (int)(onA & 15), "
           "(int)min(max((gA.s - (gA.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
-        e(f"        vt::realign<NL, NWC, {NT}>(curB, llrB, (int)(onB & 15), "
+        e(f"        vt::realign<NL, NWC, {NT}>(curB, llrB((c + 1) & 1), (int)(onB & 15), "
           "(int)min(max((gB.s - (gB.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
         e("      }")
         e("    }")
@@ -299,9 +321,13 @@ class Gen16:
         e("    tbA.start(gA, jA, actA, ng, a.N);")
         e("    tbB.start(gB, jB, actB, ng, a.N);")
         if self.GPB % 2 == 0:
+            e("    txa = parity ? a.nbs - 1 + a.b_lo : -a.b_lo;")
+            e("    txs = parity ? -1 : 1;")
             e("    tb_begin(tbA, cA0, cA1);")
             e("    tb_begin(tbB, cB0, cB1);")
         else:
+            e("    txa = parity ? a.nbs - 1 + a.b_lo : -a.b_lo;")
+            e("    txs = parity ? -1 : 1;")
             e("    tb_begin(tbA, nxtA, aftA);")
             e("    tb_begin(tbB, nxtB, aftB);")
         e("    parity_prev = parity;")

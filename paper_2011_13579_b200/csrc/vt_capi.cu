@@ -72,12 +72,13 @@ const KernelEntry* registry(int* n) {
   return table;
 }
 
-// Kernel variant: "s32" (default) or "16x2" (VT_KERNEL_VARIANT=16x2: two windows per
-// thread in packed 16-bit halves, where a 16x2 kernel exists for the code).
+// Kernel variant: "16x2" (default where a 16x2 kernel exists for the code: two windows
+// per thread in packed 16-bit halves) or "s32" (VT_KERNEL_VARIANT=s32: one window per
+// thread, 32-bit metrics).
 const KernelEntry* find(const vt_code* c) {
   if (!c) return nullptr;
   const char* env = getenv("VT_KERNEL_VARIANT");
-  const bool want16 = env && strcmp(env, "16x2") == 0;
+  const bool want16 = !(env && strcmp(env, "s32") == 0);
   int n;
   const KernelEntry* t = registry(&n);
   const KernelEntry* best = nullptr;

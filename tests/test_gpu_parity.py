@@ -157,11 +157,13 @@ def test_final_metrics_match_oracle(vt):
     np.testing.assert_array_equal(metric, want_metric.astype(np.float64))
 
 
+@pytest.mark.parametrize("variant", ["16x2", "s32"])
 @pytest.mark.parametrize("code", ["k7r2", "k7r3"])
 @pytest.mark.parametrize("fv", [(256, 42), (100, 20), (37, 5)])
-def test_packed_16x2_variant_matches_oracle(vt, code, fv, monkeypatch):
-    """The two-windows-per-thread 16x2 kernels (VT_KERNEL_VARIANT=16x2) are bit-exact too."""
-    monkeypatch.setenv("VT_KERNEL_VARIANT", "16x2")
+def test_kernel_variants_match_oracle(vt, code, fv, variant, monkeypatch):
+    """Both K=7 kernel forms are bit-exact: the default two-windows-per-thread 16x2
+    kernels and the one-window-per-thread s32 kernels (VT_KERNEL_VARIANT=s32)."""
+    monkeypatch.setenv("VT_KERNEL_VARIANT", variant)
     k, gens = code_params(CODES, code)
     spec = vt.CodeSpec(k, gens)
     f, v = fv
