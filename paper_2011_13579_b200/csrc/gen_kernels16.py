@@ -117,6 +117,34 @@ class Gen16:
         self.lines.extend(body)
         return outs
 
+    def tb_step_both(self, ind: str, p: int) -> None:
+        """Branch-free traceback step of both windows of the previous tile (shared
+        group counter tbb; buffers qA{p}/qB{p} hold the 8-state word pairs of group
+        tbb).  Consumes group tbb, then prefetches group tbb-1's pairs into the same
+        buffers (two steps of slack: the candidates of a group are 2^L consecutive
+        states).  Loads are issued unconditionally (clamped to a stored group), so
+        the step has no branches and ptxas interleaves it with the ACS work."""
+        L, S = self.L, self.S
+        e = self.emit
+        fm = (1 << L) - 1
+        e(f"{ind}{{  // traceback step (previous tile, both windows)")
+        e(f"{ind}  const bool go = tbb >= a.b_lo;")
+        e(f"{ind}  const uint32_t lA = tbA.j & 7u, lB = tbB.j & 7u;")
+        e(f"{ind}  const uint32_t wA = (lA & 4u) ? qA{p}.y : qA{p}.x;")
+        e(f"{ind}  const uint32_t wB = (lB & 4u) ? qB{p}.y : qB{p}.x;")
+        e(f"{ind}  const uint32_t hA = (wA >> ({L}u * (lA & 3u))) & {fm}u;")
+        e(f"{ind}  const uint32_t hB = (wB >> (16u + {L}u * (lB & 3u))) & {fm}u;")
+        e(f"{ind}  if (go) {{")
+        e(f"{ind}    tbA.step(hA);")
+        e(f"{ind}    tbB.step(hB);")
+        e(f"{ind}    --tbb;")
+        e(f"{ind}  }}")
+        e(f"{ind}  const uint32_t xo = (uint32_t)(txa + txs * max(tbb - 1, a.b_lo)) * {S // 16 * NT * 16}u;")
+        e(f"{ind}  const uint32_t bA = (tbA.j << {L}) & {S - 8}u, bB = (tbB.j << {L}) & {S - 8}u;")
+        e(f"{ind}  qA{p} = __ldcg(reinterpret_cast<const uint2*>(slotc + xo + (bA >> 4) * {NT * 16}u + (bA & 8u)));")
+        e(f"{ind}  qB{p} = __ldcg(reinterpret_cast<const uint2*>(slotc + xo + (bB >> 4) * {NT * 16}u + (bB & 8u)));")
+        e(f"{ind}}}")
+
     def group_end(self, ind: str, ge: int = 0) -> None:
         """Renormalisation, traceback steps, history fields -> scratch + clear.
         ge = index of this group end inside the loop body."""
@@ -140,9 +168,7 @@ class Gen16:
         e(f"{ind}// one traceback step per window of the previous tile (fields prefetched two groups")
         e(f"{ind}// ahead: the 2^L candidate states of a group are consecutive)")
         if self.GPB % 2 == 0:  # static buffer alternation: no register copy of an in-flight load
-            p = ge % 2
-            e(f"{ind}tb_step2(tbA, cA{p}, 0);")
-            e(f"{ind}tb_step2(tbB, cB{p}, 16);")
+            self.tb_step_both(ind, ge % 2)
         else:
             e(f"{ind}tb_advance(tbA, nxtA, aftA, 0);")
             e(f"{ind}tb_advance(tbB, nxtB, aftB, 16);")
@@ -203,7 +229,9 @@ class Gen16:
         e("  tbA.active = tbB.active = false;")
         e("  int parity_prev = 0, parity = 0;")
         e("  uint2 nxtA = make_uint2(0u, 0u), aftA = nxtA, nxtB = nxtA, aftB = nxtA;")
-        e("  uint2 cA0 = nxtA, cA1 = nxtA, cB0 = nxtA, cB1 = nxtA;  // two-deep prefetch buffers (static roles)")
+        e("  uint2 qA0 = nxtA, qA1 = nxtA, qB0 = nxtA, qB1 = nxtA;  // two-deep prefetch buffers (static roles)")
+        e("  int tbb = -1;  // next group of the previous tile to trace (both windows step in lockstep)")
+        e("  const char* const slotc = reinterpret_cast<const char*>(slot);")
         e("  // history words of group grp: 4 states per 32-bit word (L bits each, +16 for window B);")
         e("  // cand(grp, base): the 8-byte word pair holding states base..base+7 (base % 8 == 0)")
         e("  // traced tile: group grp sits at slot position x = txa + txs * grp (tiles alternate the order)")
@@ -300,8 +328,13 @@ class Gen16:
         e("    }")
         e("    // the previous tile's remaining traceback steps, then its unstored tail")
         if self.GPB % 2 == 0:
-            e("    while (tbA.running && tbA.b >= a.b_lo) { tb_step2(tbA, cA0, 0); tb_step2(tbA, cA1, 0); tbA.settle(a); }")
-            e("    while (tbB.running && tbB.b >= a.b_lo) { tb_step2(tbB, cB0, 16); tb_step2(tbB, cB1, 16); tbB.settle(a); }")
+            e("    while (tbb >= a.b_lo) {")
+            self.tb_step_both("      ", 0)
+            self.tb_step_both("      ", 1)
+            e("      tbA.settle(a);")
+            e("      tbB.settle(a);")
+            e("    }")
+            e("    tbA.b = tbB.b = tbb;")
         else:
             e("    while (tbA.running && tbA.b >= a.b_lo) tb_advance(tbA, nxtA, aftA, 0);")
             e("    while (tbB.running && tbB.b >= a.b_lo) tb_advance(tbB, nxtB, aftB, 16);")
@@ -323,8 +356,17 @@ class Gen16:
         if self.GPB % 2 == 0:
             e("    txa = parity ? a.nbs - 1 + a.b_lo : -a.b_lo;")
             e("    txs = parity ? -1 : 1;")
-            e("    tb_begin(tbA, cA0, cA1);")
-            e("    tb_begin(tbB, cB0, cB1);")
+            e("    tbb = ng - 1;")
+            e(f"    {{  // prefetch the last two groups: group ng-1 holds the final state, group ng-2 its candidates")
+            e(f"      const uint32_t x1 = (uint32_t)(txa + txs * max(tbb, a.b_lo)) * {S // 16 * NT * 16}u;")
+            e(f"      const uint32_t x0 = (uint32_t)(txa + txs * max(tbb - 1, a.b_lo)) * {S // 16 * NT * 16}u;")
+            e(f"      const uint32_t cA = jA & {S - 8}u, cB = jB & {S - 8}u;")
+            e(f"      const uint32_t dA = (jA << {L}) & {S - 8}u, dB = (jB << {L}) & {S - 8}u;")
+            e(f"      qA0 = __ldcg(reinterpret_cast<const uint2*>(slotc + x1 + (cA >> 4) * {NT * 16}u + (cA & 8u)));")
+            e(f"      qB0 = __ldcg(reinterpret_cast<const uint2*>(slotc + x1 + (cB >> 4) * {NT * 16}u + (cB & 8u)));")
+            e(f"      qA1 = __ldcg(reinterpret_cast<const uint2*>(slotc + x0 + (dA >> 4) * {NT * 16}u + (dA & 8u)));")
+            e(f"      qB1 = __ldcg(reinterpret_cast<const uint2*>(slotc + x0 + (dB >> 4) * {NT * 16}u + (dB & 8u)));")
+            e("    }")
         else:
             e("    txa = parity ? a.nbs - 1 + a.b_lo : -a.b_lo;")
             e("    txs = parity ? -1 : 1;")
@@ -334,8 +376,13 @@ class Gen16:
         e("  }")
         e("  // traceback of the CTA's last tile")
         if self.GPB % 2 == 0:
-            e("  while (tbA.running && tbA.b >= a.b_lo) { tb_step2(tbA, cA0, 0); tb_step2(tbA, cA1, 0); tbA.settle(a); }")
-            e("  while (tbB.running && tbB.b >= a.b_lo) { tb_step2(tbB, cB0, 16); tb_step2(tbB, cB1, 16); tbB.settle(a); }")
+            e("  while (tbb >= a.b_lo) {")
+            self.tb_step_both("    ", 0)
+            self.tb_step_both("    ", 1)
+            e("    tbA.settle(a);")
+            e("    tbB.settle(a);")
+            e("  }")
+            e("  tbA.b = tbB.b = tbb;")
         else:
             e("  while (tbA.running && tbA.b >= a.b_lo) tb_advance(tbA, nxtA, aftA, 0);")
             e("  while (tbB.running && tbB.b >= a.b_lo) tb_advance(tbB, nxtB, aftB, 16);")

@@ -36,3 +36,22 @@ if "--regions" in sys.argv:
     out.append((start, ninst, cur, smp))
     for start, ninst, n, smp in sorted(out, key=lambda x: -x[1] * x[2])[:30]:
         print(f"{start} len {ninst:5d} x {n:12,d} = {ninst*n:14,d}  samples {smp}")
+
+if "--stalls" in sys.argv:
+    # top instructions per stall reason
+    reasons = ["stall_long_sb", "stall_wait", "stall_no_inst", "stall_math", "stall_dispatch", "stall_branch_resolving", "stall_short_sb", "stall_lg"]
+    for rs in reasons:
+        if rs not in ix:
+            continue
+        tot_r = 0; items = []
+        for r in data:
+            try:
+                v = int(r[ix[rs]])
+            except Exception:
+                continue
+            tot_r += v
+            items.append((v, r[ix["Address"]][-5:], r[ix["Source"]].strip()[:70]))
+        items.sort(reverse=True)
+        print(f"== {rs}: {tot_r}")
+        for v, a, s in items[:6]:
+            print(f"   {v:7d} {a} {s}")
