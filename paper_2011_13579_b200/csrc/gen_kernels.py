@@ -367,7 +367,7 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
     os.makedirs(outdir, exist_ok=True)
     files = []
     reg = ["// GENERATED by gen_kernels.py -- kernel registry:",
-           "// VT_KERNEL(fn, K, B, lanes/window T, windows/thread, SL, chunk CH, history group BL, uint4/group SQ, {gens})",
+           "// VT_KERNEL(fn, fn without final metrics or nullptr, dynamic smem bytes, K, B, lanes/window T, windows/thread, SL, chunk CH, history group BL, uint4/group SQ, {gens})",
            ""]
     decl = ["// GENERATED by gen_kernels.py -- kernel declarations", '#include "../vt_common.cuh"', ""]
     for name, (K, polys) in codes.items():
@@ -382,7 +382,7 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
         files.append(path)
         gl = ", ".join(f"{x}u" for x in gens)
         decl.append(f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);')
-        reg.append(f"VT_KERNEL(vtk_{name}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, {g.SQ}, {{{gl}}})")
+        reg.append(f"VT_KERNEL(vtk_{name}, nullptr, 0, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, {g.SQ}, {{{gl}}})")
         if K == 7:  # packed 16x2 variant: two windows per thread
             import sys
             here = os.path.dirname(os.path.abspath(__file__))
@@ -397,7 +397,8 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
                     fh.write(src16)
             files.append(path16)
             decl.append(f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a);')
-            reg.append(f"VT_KERNEL(vtk16_{name}, {K}, {len(gens)}, 1, 2, {g16.S}, {g16.CH}, {g16.L}, "
+            decl.append(f'extern "C" __global__ void vtk16nf_{name}(const vt::StreamArgs a);')
+            reg.append(f"VT_KERNEL(vtk16_{name}, &vtk16nf_{name}, {g16.SMEM}, {K}, {len(gens)}, 1, 2, {g16.S}, {g16.CH}, {g16.L}, "
                        f"{g16.S // 16}, {{{gl}}})")
     for fname, lines in (("registry.inc", reg), ("registry_decl.inc", decl)):
         rpath = os.path.join(outdir, fname)

@@ -61,6 +61,8 @@ class Gen16:
         while self.NWC + 4 > 4 * self.NL:
             self.NL += 1
         self.lines: list[str] = []
+        ring = self.TBD * (self.S // 16) if self.GPB % 2 == 0 else 0
+        self.SMEM = (4 * self.NL + ring) * NT * 16  # dynamic shared memory bytes
 
     def pattern(self, i: int, u: int) -> int:
         reg = (u << self.k) | i
@@ -117,21 +119,40 @@ class Gen16:
         self.lines.extend(body)
         return outs
 
-    def tb_step_both(self, ind: str, p: int) -> None:
-        """Branch-free traceback step of both windows of the previous tile (shared
-        group counter tbb; buffers qA{p}/qB{p} hold the 8-state word pairs of group
-        tbb).  Consumes group tbb, then prefetches group tbb-1's pairs into the same
-        buffers (two steps of slack: the candidates of a group are 2^L consecutive
-        states).  Loads are issued unconditionally (clamped to a stored group), so
-        the step has no branches and ptxas interleaves it with the ACS work."""
-        L, S = self.L, self.S
+    TBD = 4  # traceback ring depth (groups prefetched ahead into shared memory)
+
+    def tb_fetch(self, ind: str, grp: str, ring: str) -> None:
+        """cp.async the whole history group `grp` (clamped to a stored group) of this
+        thread's slot into ring entry `ring`, and commit (one commit per step)."""
+        S, SQ = self.S, self.S // 16
+        e = self.emit
+        e(f"{ind}{{")
+        e(f"{ind}  const uint32_t xo = (uint32_t)(txa + txs * max({grp}, a.b_lo)) * {SQ * NT * 16}u;")
+        e(f"{ind}  uint4* const dst = s_tb + ({ring}) * {SQ * NT} + tid;")
+        for q in range(SQ):
+            e(f"{ind}  vt::cp_async16(dst + {q * NT}, slotc + xo + {q * NT * 16}u, 16, 0);")
+        e(f"{ind}  vt::cp_async_commit();")
+        e(f"{ind}}}")
+
+    def tb_step_both(self, ind: str, p: int = 0) -> None:
+        """Traceback step of both windows of the previous tile (shared group counter
+        tbb).  The whole history group is prefetched TBD steps ahead into a per-thread
+        shared-memory ring (cp.async: no data dependency, so DRAM latency is covered
+        by TBD group ends of ACS work); the dependent walk then only touches shared
+        memory.  Branch-free apart from the uniform `go` predicate."""
+        L, S, SQ = self.L, self.S, self.S // 16
         e = self.emit
         fm = (1 << L) - 1
         e(f"{ind}{{  // traceback step (previous tile, both windows)")
+        e(f"{ind}  vt::cp_async_wait_group<{self.TBD - 1}>();")
         e(f"{ind}  const bool go = tbb >= a.b_lo;")
+        e(f"{ind}  const char* const rs = reinterpret_cast<const char*>(s_tb + tbr * {SQ * NT} + tid);")
+        e(f"{ind}  const uint32_t cA = tbA.j & {S - 8}u, cB = tbB.j & {S - 8}u;")
+        e(f"{ind}  const uint2 qa = *reinterpret_cast<const uint2*>(rs + (cA >> 4) * {NT * 16}u + (cA & 8u));")
+        e(f"{ind}  const uint2 qb = *reinterpret_cast<const uint2*>(rs + (cB >> 4) * {NT * 16}u + (cB & 8u));")
         e(f"{ind}  const uint32_t lA = tbA.j & 7u, lB = tbB.j & 7u;")
-        e(f"{ind}  const uint32_t wA = (lA & 4u) ? qA{p}.y : qA{p}.x;")
-        e(f"{ind}  const uint32_t wB = (lB & 4u) ? qB{p}.y : qB{p}.x;")
+        e(f"{ind}  const uint32_t wA = (lA & 4u) ? qa.y : qa.x;")
+        e(f"{ind}  const uint32_t wB = (lB & 4u) ? qb.y : qb.x;")
         e(f"{ind}  const uint32_t hA = (wA >> ({L}u * (lA & 3u))) & {fm}u;")
         e(f"{ind}  const uint32_t hB = (wB >> (16u + {L}u * (lB & 3u))) & {fm}u;")
         e(f"{ind}  if (go) {{")
@@ -139,10 +160,8 @@ class Gen16:
         e(f"{ind}    tbB.step(hB);")
         e(f"{ind}    --tbb;")
         e(f"{ind}  }}")
-        e(f"{ind}  const uint32_t xo = (uint32_t)(txa + txs * max(tbb - 1, a.b_lo)) * {S // 16 * NT * 16}u;")
-        e(f"{ind}  const uint32_t bA = (tbA.j << {L}) & {S - 8}u, bB = (tbB.j << {L}) & {S - 8}u;")
-        e(f"{ind}  qA{p} = __ldcg(reinterpret_cast<const uint2*>(slotc + xo + (bA >> 4) * {NT * 16}u + (bA & 8u)));")
-        e(f"{ind}  qB{p} = __ldcg(reinterpret_cast<const uint2*>(slotc + xo + (bB >> 4) * {NT * 16}u + (bB & 8u)));")
+        self.tb_fetch(ind + "  ", f"tbb - {self.TBD - 1}", "tbr")
+        e(f"{ind}  tbr = (tbr + 1) & {self.TBD - 1};")
         e(f"{ind}}}")
 
     def group_end(self, ind: str, ge: int = 0) -> None:
@@ -155,15 +174,17 @@ class Gen16:
         e(f"{ind}// ---- group end")
         e(f"{ind}// renormalise the next group by Lambda_0 - S_b (per window half); from the fresh")
         e(f"{ind}// state-0 metric (history masked), so the chain overlaps the rest of the group end")
-        e(f"{ind}offA += pendA;")
-        e(f"{ind}offB += pendB;")
+        if self.fm:
+            e(f"{ind}offA += pendA;")
+            e(f"{ind}offB += pendB;")
         e(f"{ind}{{")
         e(f"{ind}  const uint32_t r0 = m0 & {lm:#x}u;")
         e(f"{ind}  const uint32_t rr = vt::vadd2(r0, {((-(self.Sb << L)) & 0xFFFF) * 0x10001:#x}u);")
         e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);  // -R per half, mod 2^16 (fused-add operand)")
         e(f"{ind}  negE = {(self.Sb << L) * 0x10001:#x}u - r0;  // -R as a packed integer (IMAD operand)")
-        e(f"{ind}  pendA = (int64_t)((r0 & 0xFFFFu) >> {L}) - {self.Sb};")
-        e(f"{ind}  pendB = (int64_t)(r0 >> {16 + L}) - {self.Sb};")
+        if self.fm:
+            e(f"{ind}  pendA = (int64_t)((r0 & 0xFFFFu) >> {L}) - {self.Sb};")
+            e(f"{ind}  pendB = (int64_t)(r0 >> {16 + L}) - {self.Sb};")
         e(f"{ind}}}")
         e(f"{ind}// one traceback step per window of the previous tile (fields prefetched two groups")
         e(f"{ind}// ahead: the 2^L candidate states of a group are consecutive)")
@@ -204,20 +225,33 @@ class Gen16:
                     self.emit(f"{ind}{arr}[{i}] = __funnelshift_r({a}, {b}, {8 * rb});")
 
     def kernel(self) -> str:
-        K, B, S, L, P, CH, NL, NWC = self.K, self.B, self.S, self.L, self.P, self.CH, self.NL, self.NWC
-        SQ = S // 16  # uint4 of history words per group per thread
-        name = f"vtk16_{self.name}"
+        """Both variants: vtk16_<code> (tracks final metrics when a.final_metric is set)
+        and vtk16nf_<code> (no final-metric bookkeeping: fewer live registers)."""
+        self.lines = []
         e = self.emit
         e("// GENERATED by gen_kernels16.py -- do not edit.")
-        e(f"// code {self.name}: K={K}, generators (octal) {', '.join(oct(g)[2:] for g in self.gens)}; "
-          f"two windows per thread (16x2 halves), {L}-bit history groups, {P}-stage body, {CH}-stage chunks")
+        e(f"// code {self.name}: K={self.K}, generators (octal) {', '.join(oct(g)[2:] for g in self.gens)}; "
+          f"two windows per thread (16x2 halves), {self.L}-bit history groups, {self.P}-stage body, {self.CH}-stage chunks")
         e('#include "../vt_common.cuh"')
         e("")
+        for fm in (True, False):
+            self.fm = fm
+            self.kernel_one(f"vtk16_{self.name}" if fm else f"vtk16nf_{self.name}")
+        return "\n".join(self.lines)
+
+    def kernel_one(self, name: str) -> None:
+        K, B, S, L, P, CH, NL, NWC = self.K, self.B, self.S, self.L, self.P, self.CH, self.NL, self.NWC
+        SQ = S // 16  # uint4 of history words per group per thread
+        e = self.emit
         e(f'extern "C" __global__ void __launch_bounds__({NT}, {MINB16}) {name}(const vt::StreamArgs a) {{')
         e(f"  constexpr int B = {B}, K = {K}, CH = {CH}, NL = {NL}, NWC = {NWC};")
         e("  const int tid = threadIdx.x;")
-        e(f"  // LLR staging: 2 buffers (chunk parity) x 2 windows x NL uint4 per thread (column layout)")
-        e(f"  __shared__ __align__(16) uint4 s_llr[4 * NL * {NT}];")
+        e(f"  // dynamic shared memory: LLR staging, 2 buffers (chunk parity) x 2 windows x NL uint4 per")
+        e(f"  // thread (column layout), then the traceback ring: TBD x SQ uint4 per thread")
+        e("  extern __shared__ __align__(16) uint4 smem_dyn[];")
+        e("  uint4* const s_llr = smem_dyn;")
+        e(f"  uint4* const s_tb = smem_dyn + 4 * NL * {NT};  // (even GPB only)")
+        e("  (void)s_tb;")
         e("  const uint64_t pol_last = vt::policy_evict_last();")
         e("  const int64_t nwin = a.w1 - a.w0;")
         e("  const int64_t buf_bytes = (a.st1 - a.st0) * B;")
@@ -229,13 +263,13 @@ class Gen16:
         e("  tbA.active = tbB.active = false;")
         e("  int parity_prev = 0, parity = 0;")
         e("  uint2 nxtA = make_uint2(0u, 0u), aftA = nxtA, nxtB = nxtA, aftB = nxtA;")
-        e("  uint2 qA0 = nxtA, qA1 = nxtA, qB0 = nxtA, qB1 = nxtA;  // two-deep prefetch buffers (static roles)")
         e("  int tbb = -1;  // next group of the previous tile to trace (both windows step in lockstep)")
+        e("  int tbr = 0;   // traceback ring entry holding group tbb")
         e("  const char* const slotc = reinterpret_cast<const char*>(slot);")
         e("  // history words of group grp: 4 states per 32-bit word (L bits each, +16 for window B);")
         e("  // cand(grp, base): the 8-byte word pair holding states base..base+7 (base % 8 == 0)")
         e("  // traced tile: group grp sits at slot position x = txa + txs * grp (tiles alternate the order)")
-        e("  int txa = 0, txs = 1;")
+        e("  int txa = -a.b_lo, txs = 1;  // (initial values keep the idle prefetches inside the slot)")
         e("  auto cand = [&](int grp, uint32_t base) -> uint2 {")
         e(f"    const uint32_t off = (uint32_t)(txa + txs * grp) * {SQ * NT * 16}u + (base >> 4) * {NT * 16}u + (base & 8u);")
         e("    return __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(slot) + off));")
@@ -270,7 +304,8 @@ class Gen16:
         e("    const int64_t oA = (gA.g0 - a.st0) * B, oB = (gB.g0 - a.st0) * B;")
         e("    " + " ".join(f"uint32_t m{j} = 0;" for j in range(S)))
         e("    uint32_t negR = 0, negE = 0;")
-        e("    int64_t offA = 0, offB = 0, pendA = 0, pendB = 0;")
+        if self.fm:
+            e("    int64_t offA = 0, offB = 0, pendA = 0, pendB = 0;")
         e("    uint32_t curA[NWC], curB[NWC];")
         e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole bodies of it")
         e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
@@ -280,13 +315,12 @@ class Gen16:
         e("    // chunks are staged two ahead (cp.async groups): chunk k lives in buffer k & 1")
         e(f"    vt::stage_llr<NL, {NT}>(llrA(0), a.llr, buf_bytes, oA0, 0);")
         e(f"    vt::stage_llr<NL, {NT}>(llrB(0), a.llr, buf_bytes, oB0, 0);")
-        e("    vt::cp_async_commit();")
         e("    if (a.nc > 1) {")
         e(f"      vt::stage_llr<NL, {NT}>(llrA(1), a.llr, buf_bytes, oA + (int64_t)CH * B, 0);")
         e(f"      vt::stage_llr<NL, {NT}>(llrB(1), a.llr, buf_bytes, oB + (int64_t)CH * B, 0);")
         e("    }")
         e("    vt::cp_async_commit();")
-        e("    vt::cp_async_wait_group<1>();")
+        e("    vt::cp_async_wait_group<0>();")
         e(f"    vt::realign<NL, NWC, {NT}>(curA, llrA(0), (int)(oA0 & 15), "
           f"(int)min(max((gA.s - gA.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
         e(f"    vt::realign<NL, NWC, {NT}>(curB, llrB(0), (int)(oB0 & 15), "
@@ -299,7 +333,10 @@ class Gen16:
         e(f"        vt::stage_llr<NL, {NT}>(llrA(c & 1), a.llr, buf_bytes, onA + (int64_t)CH * B, 0);")
         e(f"        vt::stage_llr<NL, {NT}>(llrB(c & 1), a.llr, buf_bytes, onB + (int64_t)CH * B, 0);")
         e("      }")
-        e("      vt::cp_async_commit();")
+        if self.GPB % 2:
+            e("      vt::cp_async_commit();")
+        else:
+            e("      // (no commit here: the staging rides on the next traceback step's commit group)")
         e("#pragma unroll 1")
         e(f"      for (int it = it_start; it < {CH_BODIES}; ++it) {{")
         names = [f"m{j}" for j in range(S)]
@@ -319,7 +356,10 @@ class Gen16:
         e("      tbA.settle(a);  // whole words of the previous tile's traceback")
         e("      tbB.settle(a);")
         e("      if (c + 1 < a.nc) {")
-        e("        vt::cp_async_wait_group<1>();")
+        if self.GPB % 2:
+            e("        vt::cp_async_wait_group<1>();")
+        else:
+            e(f"        vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 was committed >= 4 steps ago")
         e(f"        vt::realign<NL, NWC, {NT}>(curA, llrA((c + 1) & 1), (int)(onA & 15), "
           "(int)min(max((gA.s - (gA.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
         e(f"        vt::realign<NL, NWC, {NT}>(curB, llrB((c + 1) & 1), (int)(onB & 15), "
@@ -346,27 +386,21 @@ class Gen16:
             e(f"    bestA = max(bestA, ((m{j} & 0xFFFFu) << 8) | {S - 1 - j}u);")
             e(f"    bestB = max(bestB, ((m{j} >> 16) << 8) | {S - 1 - j}u);")
         e(f"    const uint32_t jA = {S - 1}u - (bestA & 0xFFu), jB = {S - 1}u - (bestB & 0xFFu);")
-        e("    if (a.final_metric) {")
-        e(f"      const int64_t bias = ((int64_t)a.nc * CH - (int64_t)it0 * {P}) * {self.dmax};")
-        e(f"      if (actA) a.final_metric[wa] = (int64_t)(bestA >> {8 + L}) + offA - bias;")
-        e(f"      if (actB) a.final_metric[wb] = (int64_t)(bestB >> {8 + L}) + offB - bias;")
-        e("    }")
+        if self.fm:
+          e("    if (a.final_metric) {")
+          e(f"      const int64_t bias = ((int64_t)a.nc * CH - (int64_t)it0 * {P}) * {self.dmax};")
+          e(f"      if (actA) a.final_metric[wa] = (int64_t)(bestA >> {8 + L}) + offA - bias;")
+          e(f"      if (actB) a.final_metric[wb] = (int64_t)(bestB >> {8 + L}) + offB - bias;")
+          e("    }")
         e("    tbA.start(gA, jA, actA, ng, a.N);")
         e("    tbB.start(gB, jB, actB, ng, a.N);")
         if self.GPB % 2 == 0:
             e("    txa = parity ? a.nbs - 1 + a.b_lo : -a.b_lo;")
             e("    txs = parity ? -1 : 1;")
             e("    tbb = ng - 1;")
-            e(f"    {{  // prefetch the last two groups: group ng-1 holds the final state, group ng-2 its candidates")
-            e(f"      const uint32_t x1 = (uint32_t)(txa + txs * max(tbb, a.b_lo)) * {S // 16 * NT * 16}u;")
-            e(f"      const uint32_t x0 = (uint32_t)(txa + txs * max(tbb - 1, a.b_lo)) * {S // 16 * NT * 16}u;")
-            e(f"      const uint32_t cA = jA & {S - 8}u, cB = jB & {S - 8}u;")
-            e(f"      const uint32_t dA = (jA << {L}) & {S - 8}u, dB = (jB << {L}) & {S - 8}u;")
-            e(f"      qA0 = __ldcg(reinterpret_cast<const uint2*>(slotc + x1 + (cA >> 4) * {NT * 16}u + (cA & 8u)));")
-            e(f"      qB0 = __ldcg(reinterpret_cast<const uint2*>(slotc + x1 + (cB >> 4) * {NT * 16}u + (cB & 8u)));")
-            e(f"      qA1 = __ldcg(reinterpret_cast<const uint2*>(slotc + x0 + (dA >> 4) * {NT * 16}u + (dA & 8u)));")
-            e(f"      qB1 = __ldcg(reinterpret_cast<const uint2*>(slotc + x0 + (dB >> 4) * {NT * 16}u + (dB & 8u)));")
-            e("    }")
+            e("    tbr = 0;")
+            for r in range(self.TBD):
+                self.tb_fetch("    ", f"tbb - {r}", f"{r}")
         else:
             e("    txa = parity ? a.nbs - 1 + a.b_lo : -a.b_lo;")
             e("    txs = parity ? -1 : 1;")
@@ -390,4 +424,3 @@ class Gen16:
         e("  if (tbB.running) tbB.drain_unstored(a);")
         e("}")
         e("")
-        return "\n".join(self.lines)

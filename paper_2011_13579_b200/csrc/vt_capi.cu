@@ -56,10 +56,12 @@ struct KernelEntry {
   int K, B, T, WPT, SL, CH, BL, SQ;
   uint32_t gens[VT_MAX_OUTPUTS];
   const void* fn;
+  const void* fn_nofm;  // variant without final-metric bookkeeping (nullptr: use fn)
+  int smem;             // dynamic shared memory bytes per CTA
 };
 
-#define VT_KERNEL(fn_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, ...) \
-  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, __VA_ARGS__, (const void*)&fn_},
+#define VT_KERNEL(fn_, fnnf_, smem_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, ...) \
+  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, __VA_ARGS__, (const void*)&fn_, (const void*)(fnnf_), smem_},
 }  // namespace
 #include "gen/registry_decl.inc"
 namespace {
@@ -107,11 +109,20 @@ int device_sms() {
   return sms;
 }
 
+// opt the kernels into their dynamic shared memory (above the 48 KB default); idempotent
+void prepare(const KernelEntry* k) {
+  if (k->smem > 0) {
+    cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem);
+    if (k->fn_nofm) cudaFuncSetAttribute(k->fn_nofm, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem);
+  }
+}
+
 int ctas_per_sm(const KernelEntry* k) {
   const char* env = getenv("VT_CTAS_PER_SM");
   if (env && atoi(env) > 0) return atoi(env);
+  prepare(k);
   int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, kNT, 0) != cudaSuccess || occ < 1) occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, kNT, k->smem) != cudaSuccess || occ < 1) occ = 1;
   return std::min(occ, 4);
 }
 
@@ -190,7 +201,9 @@ int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, 
   a.b_lo = g.b_lo;
   a.nbs = g.nbs;
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchKernel(k->fn, dim3((unsigned)grid), dim3(kNT), args, 0, (cudaStream_t)stream);
+  const void* fn = (final_metric == nullptr && k->fn_nofm) ? k->fn_nofm : k->fn;
+  prepare(k);
+  cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kNT), args, (size_t)k->smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return VT_OK;
 }
