@@ -74,13 +74,19 @@ const KernelEntry* registry(int* n) {
   return table;
 }
 
-// Kernel variant: "16x2" (default where a 16x2 kernel exists for the code: two windows
-// per thread in packed 16-bit halves) or "s32" (VT_KERNEL_VARIANT=s32: one window per
-// thread, 32-bit metrics).
+// Kernel variant: "16x2" (two windows per thread in packed 16-bit halves) or "s32" (one
+// window per thread, 32-bit metrics).  Default: 16x2 where it exists with >= 3-bit history
+// groups (K=7 rate 1/2: measured faster); s32 otherwise (K=7 rate 1/3 needs 2-bit groups,
+// whose group-end work makes the 16x2 form slower).  VT_KERNEL_VARIANT=16x2|s32 forces one.
+bool prefer16(const KernelEntry* e, const char* env) {
+  if (env && strcmp(env, "s32") == 0) return false;
+  if (env && strcmp(env, "16x2") == 0) return true;
+  return e->BL >= 3;
+}
+
 const KernelEntry* find(const vt_code* c) {
   if (!c) return nullptr;
   const char* env = getenv("VT_KERNEL_VARIANT");
-  const bool want16 = !(env && strcmp(env, "s32") == 0);
   int n;
   const KernelEntry* t = registry(&n);
   const KernelEntry* best = nullptr;
@@ -89,7 +95,13 @@ const KernelEntry* find(const vt_code* c) {
     bool same = true;
     for (int b = 0; b < c->B; ++b) same = same && t[i].gens[b] == c->gens[b];
     if (!same) continue;
-    if (!best || (want16 ? t[i].WPT > best->WPT : t[i].WPT < best->WPT)) best = &t[i];
+    if (!best) {
+      best = &t[i];
+    } else {  // two entries for this code: pick by variant
+      const KernelEntry* k16 = t[i].WPT > best->WPT ? &t[i] : best;
+      const KernelEntry* k32 = t[i].WPT > best->WPT ? best : &t[i];
+      best = prefer16(k16, env) ? k16 : k32;
+    }
   }
   return best;
 }
