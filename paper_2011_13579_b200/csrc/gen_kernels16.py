@@ -29,7 +29,7 @@ from __future__ import annotations
 from gen_kernels import NT, parity
 
 CH_BODIES = 2  # loop bodies per LLR chunk
-MINB16 = 1  # CTAs per SM bound (3 forces a 168-register cap: spills + 1.5x scratch footprint measured 25% slower)
+MINB16 = 1  # CTAs per SM bound (3 forces a 168-register cap: spills, measured 16% slower with the ring traceback)
 
 
 def history_bits(K: int, B: int) -> int:
@@ -93,8 +93,9 @@ class Gen16:
             e(f"{ind}const uint32_t P{q}_{b} = vt::prmt(curA[{w}], curB[{w}], {sel:#x}u);")
             e(f"{ind}const uint32_t U{q}_{b} = vt::vadd2(P{q}_{b}, 0x00800080u) << {L};")
             e(f"{ind}const uint32_t N{q}_{b} = {(256 << L) * 0x10001:#x}u - U{q}_{b};")
-        outs, body, need_d, need_e = [], [], set(), set()
-        for j in range(S):
+        outs, body, need_d, need_e = [None] * S, [], set(), set()
+        # butterfly order (j, j + S/2 share predecessors i0, i1): the old metrics die in pairs
+        for j in [x for k in range(S // 2) for x in (k, k + S // 2)]:
             u = j >> (self.k - 1)
             i0 = (j << 1) & (S - 1)
             i1 = i0 | 1
@@ -104,7 +105,7 @@ class Gen16:
             nm = f"x{q}_{j}"
             body.append(f"{ind}const uint32_t {nm} = vt::vaddmax2({names[i0]}, D{q}_{p0}, "
                         f"vt::mad_u32({names[i1]}, 1u, E{q}_{p1}));")
-            outs.append(nm)
+            outs[j] = nm
         if gq == 0:
             e(f"{ind}const uint32_t kE{q} = negE + {flag} * 0x10001u;")
         for p in sorted(need_d | need_e):
