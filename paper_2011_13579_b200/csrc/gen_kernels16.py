@@ -257,8 +257,9 @@ class Gen16:
         e("  const int64_t nwin = a.w1 - a.w0;")
         e("  const int64_t buf_bytes = (a.st1 - a.st0) * B;")
         e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {SQ} * {NT} + tid;")
-        e(f"  auto llrA = [&](int buf) {{ return s_llr + (2 * buf) * NL * {NT} + tid; }};")
-        e(f"  auto llrB = [&](int buf) {{ return s_llr + (2 * buf + 1) * NL * {NT} + tid; }};")
+        e("  // per-thread rows of NL*16 bytes: [buffer][window][thread]")
+        e(f"  auto llrA = [&](int buf) {{ return reinterpret_cast<char*>(s_llr) + ((2 * buf) * {NT} + tid) * (16 * NL); }};")
+        e(f"  auto llrB = [&](int buf) {{ return reinterpret_cast<char*>(s_llr) + ((2 * buf + 1) * {NT} + tid) * (16 * NL); }};")
         e(f"  vt::TracebackLite<K, {L}> tbA, tbB;")
         e("  tbA.running = tbB.running = false;")
         e("  tbA.active = tbB.active = false;")
@@ -303,6 +304,9 @@ class Gen16:
         e(f"    const vt::Window gA = vt::window_geometry<{CH}>(a, a.w0 + (actA ? wa : nwin - 1));")
         e(f"    const vt::Window gB = vt::window_geometry<{CH}>(a, a.w0 + (actB ? wb : nwin - 1));")
         e("    const int64_t oA = (gA.g0 - a.st0) * B, oB = (gB.g0 - a.st0) * B;")
+        e("    // the window's whole staged span (16-byte words) lies inside the buffer: unchecked copies")
+        e(f"    const int64_t span = (int64_t)a.nc * CH * B + 16 * NL;")
+        e("    const bool fastA = oA >= 0 && oA + span <= buf_bytes, fastB = oB >= 0 && oB + span <= buf_bytes;")
         e("    " + " ".join(f"uint32_t m{j} = 0;" for j in range(S)))
         e("    uint32_t negR = 0, negE = 0;")
         if self.fm:
@@ -314,25 +318,25 @@ class Gen16:
         e("    int it_start = it0;")
         e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
         e("    // chunks are staged two ahead (cp.async groups): chunk k lives in buffer k & 1")
-        e(f"    vt::stage_llr<NL, {NT}>(llrA(0), a.llr, buf_bytes, oA0, 0);")
-        e(f"    vt::stage_llr<NL, {NT}>(llrB(0), a.llr, buf_bytes, oB0, 0);")
+        e(f"    vt::stage_row<NL>(llrA(0), a.llr, buf_bytes, oA0, fastA);")
+        e(f"    vt::stage_row<NL>(llrB(0), a.llr, buf_bytes, oB0, fastB);")
         e("    if (a.nc > 1) {")
-        e(f"      vt::stage_llr<NL, {NT}>(llrA(1), a.llr, buf_bytes, oA + (int64_t)CH * B, 0);")
-        e(f"      vt::stage_llr<NL, {NT}>(llrB(1), a.llr, buf_bytes, oB + (int64_t)CH * B, 0);")
+        e(f"      vt::stage_row<NL>(llrA(1), a.llr, buf_bytes, oA + (int64_t)CH * B, fastA);")
+        e(f"      vt::stage_row<NL>(llrB(1), a.llr, buf_bytes, oB + (int64_t)CH * B, fastB);")
         e("    }")
         e("    vt::cp_async_commit();")
         e("    vt::cp_async_wait_group<0>();")
-        e(f"    vt::realign<NL, NWC, {NT}>(curA, llrA(0), (int)(oA0 & 15), "
+        e(f"    vt::realign_row<NWC>(curA, llrA(0), (int)(oA0 & 15), "
           f"(int)min(max((gA.s - gA.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
-        e(f"    vt::realign<NL, NWC, {NT}>(curB, llrB(0), (int)(oB0 & 15), "
+        e(f"    vt::realign_row<NWC>(curB, llrB(0), (int)(oB0 & 15), "
           f"(int)min(max((gB.s - gB.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
         e(f"    int gidx = it0 * {self.GPB};")
         e("    // traceback of the previous tile: one group step per forward group, loads one group ahead")
         e("    for (int c = 0; c < a.nc; ++c) {")
         e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
         e("      if (c + 2 < a.nc) {")
-        e(f"        vt::stage_llr<NL, {NT}>(llrA(c & 1), a.llr, buf_bytes, onA + (int64_t)CH * B, 0);")
-        e(f"        vt::stage_llr<NL, {NT}>(llrB(c & 1), a.llr, buf_bytes, onB + (int64_t)CH * B, 0);")
+        e(f"        vt::stage_row<NL>(llrA(c & 1), a.llr, buf_bytes, onA + (int64_t)CH * B, fastA);")
+        e(f"        vt::stage_row<NL>(llrB(c & 1), a.llr, buf_bytes, onB + (int64_t)CH * B, fastB);")
         e("      }")
         if self.GPB % 2:
             e("      vt::cp_async_commit();")
@@ -361,9 +365,9 @@ class Gen16:
             e("        vt::cp_async_wait_group<1>();")
         else:
             e(f"        vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 was committed >= 4 steps ago")
-        e(f"        vt::realign<NL, NWC, {NT}>(curA, llrA((c + 1) & 1), (int)(onA & 15), "
+        e(f"        vt::realign_row<NWC>(curA, llrA((c + 1) & 1), (int)(onA & 15), "
           "(int)min(max((gA.s - (gA.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
-        e(f"        vt::realign<NL, NWC, {NT}>(curB, llrB((c + 1) & 1), (int)(onB & 15), "
+        e(f"        vt::realign_row<NWC>(curB, llrB((c + 1) & 1), (int)(onB & 15), "
           "(int)min(max((gB.s - (gB.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
         e("      }")
         e("    }")

@@ -168,6 +168,48 @@ __device__ __forceinline__ void realign(uint32_t (&out)[NWC], const uint4* smem_
   }
 }
 
+// Row-layout staging (16x2 kernels): each thread's NL staged 16-byte words are one
+// contiguous 16*NL-byte row (row stride 48 B for NL=3: the 16-byte cp.async writes of
+// 8 consecutive threads hit distinct banks).  `fast` = the whole span is inside the
+// buffer (no per-word bounds checks).
+template <int NL>
+__device__ __forceinline__ void stage_row(char* row, const int8_t* __restrict__ llr, int64_t buf_bytes, int64_t o,
+                                          bool fast) {
+  const int64_t base = (o >> 4) << 4;
+  if (fast) {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) cp_async16(row + 16 * i, llr + base + 16 * i, 16, 0);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+      const int64_t a = base + 16 * i;
+      const bool ok = (a >= 0) && (a < buf_bytes);
+      cp_async16(row + 16 * i, llr + (ok ? a : 0), ok ? 16 : 0, 0);
+    }
+  }
+}
+
+// Words [o, o + 4*NWC) of a row staged by stage_row (off = o & 15): NWC+1 aligned
+// 4-byte loads and a funnel shift by the byte misalignment; zero the first zb bytes.
+template <int NWC>
+__device__ __forceinline__ void realign_row(uint32_t (&out)[NWC], const char* row, int off, int zb) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row + (off & 12));
+  uint32_t v[NWC + 1];
+#pragma unroll
+  for (int k = 0; k <= NWC; ++k) v[k] = w[k];
+  const int r = (off & 3) * 8;
+#pragma unroll
+  for (int k = 0; k < NWC; ++k) out[k] = __funnelshift_r(v[k], v[k + 1], r);
+  if (zb > 0) {
+#pragma unroll
+    for (int k = 0; k < NWC; ++k) {
+      const int lo = zb - 4 * k;
+      if (lo >= 4) out[k] = 0u;
+      else if (lo > 0) out[k] &= 0xFFFFFFFFu << (8 * lo);
+    }
+  }
+}
+
 // LLR byte `byte` of a realigned chunk as (llr << 16), sign-extended.
 __device__ __forceinline__ int32_t llr_hi16(uint32_t word, uint32_t sh) {
   // result bytes: [0]=0, [1]=0, [2]=src byte sh, [3]=sign(src byte sh)
