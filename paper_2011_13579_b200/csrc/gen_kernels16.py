@@ -41,6 +41,22 @@ def history_bits(K: int, B: int) -> int:
     raise ValueError("no history width fits")
 
 
+def spread_weight(K: int, gens: tuple[int, ...]) -> int:
+    """Max Hamming weight of the output difference of two K-1-stage paths from the same
+    state (= encoder output weight of a nonzero input sequence from the zero state,
+    newest bit at the register MSB as codes.py:183-193): the metric spread is at most
+    256 * this for |l| <= 128."""
+    k = K - 1
+    best = 0
+    for e in range(1, 1 << k):
+        reg, w = 0, 0
+        for t in range(k):
+            reg = (reg >> 1) | (((e >> t) & 1) << k)
+            w += sum(parity(g & reg) for g in gens)
+        best = max(best, w)
+    return best
+
+
 class Gen16:
     def __init__(self, name: str, K: int, gens: tuple[int, ...]):
         self.name = name
@@ -56,6 +72,21 @@ class Gen16:
         self.GPB = self.P // self.L  # history groups per body
         self.dmax = 128 * self.B
         self.Sb = 2 * self.k * self.dmax
+        # Cheap middle stage (see stage()): needs 3-bit groups, an even number of groups
+        # per body and complementary branch patterns of the two predecessors (every
+        # generator taps the oldest register bit), and a renormalisation target
+        # Sb' >= Delta + 2*dmax with Sb' + Delta + L*2*dmax < 2^(16-L), where Delta =
+        # 256 * W is the metric-spread bound from the code's maximum output-difference
+        # weight W over K-1 stages (|l| <= 128 per LLR).
+        comp = all(self.pattern(((j << 1) & (self.S - 1)) | 1, j >> (self.k - 1)) ==
+                   self.pattern((j << 1) & (self.S - 1), j >> (self.k - 1)) ^ ((1 << self.B) - 1)
+                   for j in range(self.S))
+        delta = 256 * spread_weight(K, gens)
+        sbc = delta + 2 * self.dmax
+        self.cheap = (self.L == 3 and self.GPB % 2 == 0 and comp and
+                      sbc + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)))
+        if self.cheap:
+            self.Sb = sbc
         self.NWC = -(-self.CH * self.B // 4)
         self.NL = -(-(self.NWC * 4 + 15) // 16)
         while self.NWC + 4 > 4 * self.NL:
@@ -71,7 +102,7 @@ class Gen16:
     def emit(self, s: str = "") -> None:
         self.lines.append(s)
 
-    def stage(self, ind: str, q: int, names: list[str]) -> list[str]:
+    def stage(self, ind: str, q: int, names: list[str], defer: list | None = None) -> list[str]:
         """One radix-2 stage (body position q) for both windows.
 
         Candidate i1 is formed with a plain 32-bit IMAD (FMA pipe): every per-half
@@ -94,8 +125,82 @@ class Gen16:
             e(f"{ind}const uint32_t U{q}_{b} = vt::vadd2(P{q}_{b}, 0x00800080u) << {L};")
             e(f"{ind}const uint32_t N{q}_{b} = {(256 << L) * 0x10001:#x}u - U{q}_{b};")
         outs, body, need_d, need_e = [None] * S, [], set(), set()
+        order = [x for k in range(S // 2) for x in (k, k + S // 2)]
+        if self.cheap and gq == 1:
+            # CHEAP stage: with the i0 branch metric as a per-state offset phi_j of the
+            # stored metric (stored = true - S(p0(j))), the update needs no candidate add:
+            #   stored_j = max(m_i1 + T_p0, m_i0),  T_p0 = S(~p0) - S(p0) + 2^1 * flag
+            # (patterns of i0 and i1 are complementary).  One VIADDMNMX per state pair.
+            allp = set()
+            for j in order:
+                u = j >> (self.k - 1)
+                i0 = (j << 1) & (S - 1)
+                p0 = self.pattern(i0, u)
+                allp.add(p0)
+                allp.add(p0 ^ ((1 << B) - 1))
+                nm = f"x{q}_{j}"
+                body.append(f"{ind}const uint32_t {nm} = vt::vaddmax2({names[i0 | 1]}, T{q}_{p0}, {names[i0]});")
+                outs[j] = nm
+            for p in sorted(allp):
+                expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(B))
+                e(f"{ind}const uint32_t S{q}_{p} = {expr};")
+            full = (1 << B) - 1
+            done = set()
+            for p in sorted(allp):
+                if p in done:
+                    continue
+                pc = p ^ full
+                # per half mod 2^16: T_p = S_pc - S_p + 2f ; T_pc = -T_p + 4f
+                e(f"{ind}const uint32_t T{q}_{p} = vt::vadd2(vt::vadd2(S{q}_{pc}, ~S{q}_{p}), (1u + 2u * {flag}) * 0x10001u);")
+                e(f"{ind}const uint32_t T{q}_{pc} = vt::vadd2(~T{q}_{p}, (1u + 4u * {flag}) * 0x10001u);")
+                done |= {p, pc}
+            if defer is not None:
+                defer.extend(body)
+            else:
+                self.lines.extend(body)
+            return outs
+        if self.cheap and gq == 2:
+            # offset stage after the cheap one: state i carries phi_i = S1(p0(i)), so the
+            # addends are combos S1(class of the predecessor) + S2(branch pattern)
+            q1 = q - 1
+            combos_d, combos_e = set(), set()
+            for j in order:
+                u = j >> (self.k - 1)
+                i0 = (j << 1) & (S - 1)
+                i1 = i0 | 1
+                c0 = (self.pattern((i0 << 1) & (S - 1), i0 >> (self.k - 1)), self.pattern(i0, u))
+                c1 = (self.pattern((i1 << 1) & (S - 1), i1 >> (self.k - 1)), self.pattern(i1, u))
+                combos_d.add(c0)
+                combos_e.add(c1)
+                nm = f"x{q}_{j}"
+                body.append(f"{ind}const uint32_t {nm} = vt::vaddmax2({names[i0]}, D{q}_{c0[0]}_{c0[1]}, "
+                            f"vt::mad_u32({names[i1]}, 1u, E{q}_{c1[0]}_{c1[1]}));")
+                outs[j] = nm
+            pb_all = sorted({c[1] for c in combos_d | combos_e})
+            for p in pb_all:
+                expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(B))
+                e(f"{ind}const uint32_t S{q}_{p} = {expr};")
+            for p in sorted({c[1] for c in combos_e}):
+                e(f"{ind}const uint32_t Sf{q}_{p} = S{q}_{p} + {flag} * {(1 << gq) * 0x10001:#x}u;")
+            for pa, pb in sorted(combos_d):
+                e(f"{ind}const uint32_t D{q}_{pa}_{pb} = S{q1}_{pa} + S{q}_{pb};")
+            for pa, pb in sorted(combos_e):
+                e(f"{ind}const uint32_t E{q}_{pa}_{pb} = S{q1}_{pa} + Sf{q}_{pb};")
+            if defer is not None:
+                # interleave with the deferred cheap stage (all-ALU) so both pipes stay fed:
+                # offset-stage butterfly k and k+S/4 consume cheap butterflies 2k, 2k+1
+                h = len(defer) // 2  # butterflies
+                cheap_bf = [defer[2 * i: 2 * i + 2] for i in range(h)]
+                off_bf = [body[2 * i: 2 * i + 2] for i in range(h)]
+                for k in range(h // 2):
+                    self.lines.extend(cheap_bf[2 * k] + cheap_bf[2 * k + 1])
+                    self.lines.extend(off_bf[k] + off_bf[k + h // 2])
+                defer.clear()
+            else:
+                self.lines.extend(body)
+            return outs
         # butterfly order (j, j + S/2 share predecessors i0, i1): the old metrics die in pairs
-        for j in [x for k in range(S // 2) for x in (k, k + S // 2)]:
+        for j in order:
             u = j >> (self.k - 1)
             i0 = (j << 1) & (S - 1)
             i1 = i0 | 1
@@ -307,10 +412,12 @@ class Gen16:
         e("    // the window's whole staged span (16-byte words) lies inside the buffer: unchecked copies")
         e(f"    const int64_t span = (int64_t)a.nc * CH * B + 16 * NL;")
         e("    const bool fastA = oA >= 0 && oA + span <= buf_bytes, fastB = oB >= 0 && oB + span <= buf_bytes;")
-        e("    " + " ".join(f"uint32_t m{j} = 0;" for j in range(S)))
+        m0 = (self.Sb << L) * 0x10001 if self.cheap else 0  # cheap stages need m_i1 + T >= 0 from the start
+        e("    " + " ".join(f"uint32_t m{j} = {m0:#x}u;" for j in range(S)))
         e("    uint32_t negR = 0, negE = 0;")
         if self.fm:
-            e("    int64_t offA = 0, offB = 0, pendA = 0, pendB = 0;")
+            o0 = -self.Sb if self.cheap else 0
+            e(f"    int64_t offA = {o0}, offB = {o0}, pendA = 0, pendB = 0;")
         e("    uint32_t curA[NWC], curB[NWC];")
         e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole bodies of it")
         e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
@@ -345,11 +452,12 @@ class Gen16:
         e("#pragma unroll 1")
         e(f"      for (int it = it_start; it < {CH_BODIES}; ++it) {{")
         names = [f"m{j}" for j in range(S)]
+        deferred: list = []
         for q in range(P):
             if q % L == 0:
                 e("        // history codes only in groups whose decisions are stored (warm-up needs none)")
                 e(f"        const uint32_t cflag{q} = (gidx >= a.b_lo) ? 1u : 0u;")
-            names = self.stage("        ", q, names)
+            names = self.stage("        ", q, names, deferred if (self.cheap and q % L in (1, 2)) else None)
             if q % L == L - 1:
                 for j in range(S):
                     e(f"        m{j} = {names[j]};")
