@@ -33,6 +33,7 @@ from .decoder import (
     quantize_llr,
     workspace_bytes,
 )
+from . import fileio  # noqa: F401  (cli.py file formats)
 from .framing import DEFAULT_FRAME_LEN, DEFAULT_OVERLAP, FramePlan, Window, plan_frames
 
 __all__ = [
