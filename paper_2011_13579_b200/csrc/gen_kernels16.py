@@ -245,13 +245,12 @@ class Gen16:
         tbb).  The whole history group is prefetched TBD steps ahead into a per-thread
         shared-memory ring (cp.async: no data dependency, so DRAM latency is covered
         by TBD group ends of ACS work); the dependent walk then only touches shared
-        memory.  Branch-free apart from the uniform `go` predicate."""
+        memory.  Branch-free."""
         L, S, SQ = self.L, self.S, self.S // 16
         e = self.emit
         fm = (1 << L) - 1
         e(f"{ind}{{  // traceback step (previous tile, both windows)")
         e(f"{ind}  vt::cp_async_wait_group<{self.TBD - 1}>();")
-        e(f"{ind}  const bool go = tbb >= a.b_lo;")
         e(f"{ind}  const char* const rs = reinterpret_cast<const char*>(s_tb + tbr * {SQ * NT} + tid);")
         e(f"{ind}  const uint32_t cA = tbA.j & {S - 8}u, cB = tbB.j & {S - 8}u;")
         e(f"{ind}  const uint2 qa = *reinterpret_cast<const uint2*>(rs + (cA >> 4) * {NT * 16}u + (cA & 8u));")
@@ -261,11 +260,12 @@ class Gen16:
         e(f"{ind}  const uint32_t wB = (lB & 4u) ? qb.y : qb.x;")
         e(f"{ind}  const uint32_t hA = (wA >> ({L}u * (lA & 3u))) & {fm}u;")
         e(f"{ind}  const uint32_t hB = (wB >> (16u + {L}u * (lB & 3u))) & {fm}u;")
-        e(f"{ind}  if (go) {{")
-        e(f"{ind}    tbA.step(hA);")
-        e(f"{ind}    tbB.step(hB);")
-        e(f"{ind}    --tbb;")
-        e(f"{ind}  }}")
+        # unconditional: past the last stored group (or before the first traced tile) the
+        # walk runs on clamped junk, but those bits lie below every emit range and settle()
+        # writes nothing once a window is finished -- no branch splits the ACS block
+        e(f"{ind}  tbA.step(hA);")
+        e(f"{ind}  tbB.step(hB);")
+        e(f"{ind}  --tbb;")
         self.tb_fetch(ind + "  ", f"tbb - {self.TBD - 1}", "tbr")
         e(f"{ind}  tbr = (tbr + 1) & {self.TBD - 1};")
         e(f"{ind}}}")
@@ -367,6 +367,7 @@ class Gen16:
         e(f"  auto llrB = [&](int buf) {{ return reinterpret_cast<char*>(s_llr) + ((2 * buf + 1) * {NT} + tid) * (16 * NL); }};")
         e(f"  vt::TracebackLite<K, {L}> tbA, tbB;")
         e("  tbA.running = tbB.running = false;")
+        e("  tbA.j = tbB.j = 0u; tbA.acc = tbB.acc = 0ull; tbA.lo = tbB.lo = 0; tbA.b = tbB.b = -1;")
         e("  tbA.active = tbB.active = false;")
         e("  int parity_prev = 0, parity = 0;")
         e("  uint2 nxtA = make_uint2(0u, 0u), aftA = nxtA, nxtB = nxtA, aftB = nxtA;")
