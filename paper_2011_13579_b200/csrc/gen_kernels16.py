@@ -58,7 +58,7 @@ def spread_weight(K: int, gens: tuple[int, ...]) -> int:
 
 
 class Gen16:
-    def __init__(self, name: str, K: int, gens: tuple[int, ...]):
+    def __init__(self, name: str, K: int, gens: tuple[int, ...], tc: bool = False):
         self.name = name
         self.K = K
         self.k = K - 1
@@ -94,6 +94,13 @@ class Gen16:
         self.lines: list[str] = []
         ring = self.TBD * (self.S // 16) if self.GPB % 2 == 0 else 0
         self.SMEM = (4 * self.NL + ring) * NT * 16  # dynamic shared memory bytes
+        # tensor-core branch metrics (paper formulation): int8 LLR tile x +-8 codeword matrix
+        self.tc = tc
+        if tc:
+            assert self.cheap and self.B == 2 and self.CH * self.B <= 24 and NT == 128
+            self.TCN = self.CH * 4           # MMA N: 4 pattern sums per stage of a chunk
+            self.TCOFF = self.SMEM           # A tiles [buffer][window set] 4 KB each, B 2 KB, barriers
+            self.SMEM += 4 * 4096 + 2048 + 64
 
     def pattern(self, i: int, u: int) -> int:
         reg = (u << self.k) | i
@@ -101,6 +108,24 @@ class Gen16:
 
     def emit(self, s: str = "") -> None:
         self.lines.append(s)
+
+    def emit_S(self, ind: str, q: int, pats) -> None:
+        """Pattern sums S_p = sum_b (U or N)_b of body stage q for the patterns `pats`:
+        from the U/N terms, or (tc variant) from the chunk's tensor-core contraction
+        in TMEM (one 32x32b.x4 load per window set: the 4 pattern columns of the stage)."""
+        e = self.emit
+        pats = sorted(set(pats))
+        if not self.tc:
+            for p in pats:
+                expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(self.B))
+                e(f"{ind}const uint32_t S{q}_{p} = {expr};")
+            return
+        e(f"{ind}uint32_t ta{q}_0, ta{q}_1, ta{q}_2, ta{q}_3, tb{q}_0, tb{q}_1, tb{q}_2, tb{q}_3;")
+        e(f"{ind}vt::tc::ld4(tcA + {4 * q}u, ta{q}_0, ta{q}_1, ta{q}_2, ta{q}_3);")
+        e(f"{ind}vt::tc::ld4(tcA + {4 * q + self.TCN}u, tb{q}_0, tb{q}_1, tb{q}_2, tb{q}_3);")
+        e(f"{ind}vt::tc::wait_ld();")
+        for p in pats:  # window A in the low half, window B in the high half
+            e(f"{ind}const uint32_t S{q}_{p} = vt::prmt(ta{q}_{p}, tb{q}_{p}, 0x5410u);")
 
     def stage(self, ind: str, q: int, names: list[str], defer: list | None = None) -> list[str]:
         """One radix-2 stage (body position q) for both windows.
@@ -116,7 +141,7 @@ class Gen16:
         gq = q % L
         flag = f"cflag{q - gq}"
         e = self.emit
-        for b in range(B):
+        for b in range(B if not self.tc else 0):
             byte = q * B + b
             w, k = byte >> 2, byte & 3
             sel = k | ((8 | k) << 4) | ((4 + k) << 8) | ((12 + k) << 12)
@@ -141,9 +166,7 @@ class Gen16:
                 nm = f"x{q}_{j}"
                 body.append(f"{ind}const uint32_t {nm} = vt::vaddmax2({names[i0 | 1]}, T{q}_{p0}, {names[i0]});")
                 outs[j] = nm
-            for p in sorted(allp):
-                expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(B))
-                e(f"{ind}const uint32_t S{q}_{p} = {expr};")
+            self.emit_S(ind, q, allp)
             full = (1 << B) - 1
             done = set()
             for p in sorted(allp):
@@ -177,9 +200,7 @@ class Gen16:
                             f"vt::mad_u32({names[i1]}, 1u, E{q}_{c1[0]}_{c1[1]}));")
                 outs[j] = nm
             pb_all = sorted({c[1] for c in combos_d | combos_e})
-            for p in pb_all:
-                expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(B))
-                e(f"{ind}const uint32_t S{q}_{p} = {expr};")
+            self.emit_S(ind, q, pb_all)
             for p in sorted({c[1] for c in combos_e}):
                 e(f"{ind}const uint32_t Sf{q}_{p} = S{q}_{p} + {flag} * {(1 << gq) * 0x10001:#x}u;")
             for pa, pb in sorted(combos_d):
@@ -213,9 +234,8 @@ class Gen16:
             outs[j] = nm
         if gq == 0:
             e(f"{ind}const uint32_t kE{q} = negE + {flag} * 0x10001u;")
+        self.emit_S(ind, q, need_d | need_e)
         for p in sorted(need_d | need_e):
-            expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(B))
-            e(f"{ind}const uint32_t S{q}_{p} = {expr};")
             if p in need_d:
                 d = f"vt::vadd2(S{q}_{p}, negR)" if gq == 0 else f"S{q}_{p}"
                 e(f"{ind}const uint32_t D{q}_{p} = {d};")
@@ -340,9 +360,10 @@ class Gen16:
           f"two windows per thread (16x2 halves), {self.L}-bit history groups, {self.P}-stage body, {self.CH}-stage chunks")
         e('#include "../vt_common.cuh"')
         e("")
+        pre = "vtk16tc" if self.tc else "vtk16"
         for fm in (True, False):
             self.fm = fm
-            self.kernel_one(f"vtk16_{self.name}" if fm else f"vtk16nf_{self.name}")
+            self.kernel_one(f"{pre}_{self.name}" if fm else f"{pre}nf_{self.name}")
         return "\n".join(self.lines)
 
     def kernel_one(self, name: str) -> None:
@@ -374,6 +395,62 @@ class Gen16:
         e("  int tbb = -1;  // next group of the previous tile to trace (both windows step in lockstep)")
         e("  int tbr = 0;   // traceback ring entry holding group tbb")
         e("  const char* const slotc = reinterpret_cast<const char*>(slot);")
+        if self.tc:
+            TCN = self.TCN
+            e(f"  // ---- tensor-core branch metrics: per chunk, D[window][4*stage + pattern] = A . Bm with")
+            e(f"  // A = the window's {2 * CH} int8 LLRs of the chunk (+ a bias byte), Bm = the +-8 codeword")
+            e(f"  // matrix (+ bias row): S_p = 8 * sum_b (+-l_b) + 2048 = sum_b (U or N)_b  (tcgen05 kind::i8)")
+            e(f"  char* const s_tc = reinterpret_cast<char*>(smem_dyn) + {self.TCOFF};")
+            e("  uint64_t* const tc_bar = reinterpret_cast<uint64_t*>(s_tc + 4 * 4096 + 2048);")
+            e("  uint32_t* const tc_tm = reinterpret_cast<uint32_t*>(s_tc + 4 * 4096 + 2048 + 16);")
+            e(f"  for (int i = tid; i < {TCN} * 32; i += {NT}) {{")
+            e("    const int n = i >> 5, k = i & 31, st = n >> 2, pp = n & 3;")
+            e("    int v = 0;")
+            e(f"    if (k < {2 * CH} && (k >> 1) == st) v = ((pp >> (k & 1)) & 1) ? -8 : 8;")
+            e(f"    else if (k == {2 * CH}) v = 32;")
+            e("    s_tc[4 * 4096 + vt::tc::kmaj(n, k)] = (char)v;")
+            e("  }")
+            e(f"  for (int i = tid; i < 4 * {NT}; i += {NT})  // A rows: bias byte 64 at k = {2 * CH}, zeros after")
+            e(f"    *reinterpret_cast<uint2*>(s_tc + (i >> 7) * 4096 + vt::tc::kmaj(i & 127, {2 * CH})) = make_uint2(64u, 0u);")
+            e("  if (tid < 32) vt::tc::alloc<256>(tc_tm);")
+            e("  if (tid == 0) {")
+            e("    vt::tc::mbar_init(tc_bar, 1);")
+            e("    vt::tc::mbar_init(tc_bar + 1, 1);")
+            e('    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");')
+            e("  }")
+            e("  vt::tc::fence_proxy_async();")
+            e("  vt::tc::fence_before();")
+            e("  __syncthreads();")
+            e("  vt::tc::fence_after();")
+            e("  const uint32_t tmb = *tc_tm;")
+            e("  const uint32_t tcrow = tmb + ((uint32_t)(32 * (tid >> 5)) << 16);  // this warp's TMEM lane quarter")
+            e("  uint32_t tc_phase = 0;")
+            e("  const uint64_t tc_db = vt::tc::desc_kmaj(vt::tc::smem_u32(s_tc + 4 * 4096));")
+            e(f"  constexpr uint32_t TC_ID = vt::tc::idesc_i8({NT}, {TCN});")
+            e("  // row tid of the chunk tiles (buffer buf): the realigned LLR words of windows A and B")
+            e("  auto tc_write = [&](int buf, const uint32_t (&wa)[NWC], const uint32_t (&wb)[NWC]) {")
+            e("    char* const ta = s_tc + (2 * buf) * 4096;")
+            e("    char* const tb = ta + 4096;")
+            e("    *reinterpret_cast<uint4*>(ta + vt::tc::kmaj(tid, 0)) = make_uint4(wa[0], wa[1], wa[2], wa[3]);")
+            e("    *reinterpret_cast<uint2*>(ta + vt::tc::kmaj(tid, 16)) = make_uint2(wa[4], wa[5]);")
+            e("    *reinterpret_cast<uint4*>(tb + vt::tc::kmaj(tid, 0)) = make_uint4(wb[0], wb[1], wb[2], wb[3]);")
+            e("    *reinterpret_cast<uint2*>(tb + vt::tc::kmaj(tid, 16)) = make_uint2(wb[4], wb[5]);")
+            e("  };")
+            e("  // all rows written -> one thread issues the two MMAs of chunk buffer buf")
+            e("  auto tc_issue = [&](int buf0, int nbuf) {")
+            e("    vt::tc::fence_before();")
+            e("    vt::tc::fence_proxy_async();")
+            e("    __syncthreads();")
+            e("    if (tid == 0) {")
+            e("      vt::tc::fence_after();")
+            e("      for (int bb = buf0; bb < buf0 + nbuf; ++bb) {")
+            e("        const uint32_t ab = vt::tc::smem_u32(s_tc + (2 * bb) * 4096);")
+            e(f"        vt::tc::mma_i8(tmb + bb * 128, vt::tc::desc_kmaj(ab), tc_db, TC_ID);")
+            e(f"        vt::tc::mma_i8(tmb + bb * 128 + {TCN}, vt::tc::desc_kmaj(ab + 4096), tc_db, TC_ID);")
+            e("        vt::tc::commit(tc_bar + bb);")
+            e("      }")
+            e("    }")
+            e("  };")
         e("  // history words of group grp: 4 states per 32-bit word (L bits each, +16 for window B);")
         e("  // cand(grp, base): the 8-byte word pair holding states base..base+7 (base % 8 == 0)")
         e("  // traced tile: group grp sits at slot position x = txa + txs * grp (tiles alternate the order)")
@@ -419,10 +496,15 @@ class Gen16:
         if self.fm:
             o0 = -self.Sb if self.cheap else 0
             e(f"    int64_t offA = {o0}, offB = {o0}, pendA = 0, pendB = 0;")
-        e("    uint32_t curA[NWC], curB[NWC];")
+        if not self.tc:
+            e("    uint32_t curA[NWC], curB[NWC];")
         e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole bodies of it")
-        e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
-          f"(int64_t){CH_BODIES});")
+        if self.tc:  # warp-uniform: tcgen05.ld is .sync.aligned, so every lane must run the same bodies
+            e(f"    const int it0 = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)min(min(max(gA.s - gA.g0, (int64_t)0), "
+              f"max(gB.s - gB.g0, (int64_t)0)) / {P}, (int64_t){CH_BODIES}));")
+        else:
+            e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
+              f"(int64_t){CH_BODIES});")
         e("    int it_start = it0;")
         e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
         e("    // chunks are staged two ahead (cp.async groups): chunk k lives in buffer k & 1")
@@ -434,10 +516,26 @@ class Gen16:
         e("    }")
         e("    vt::cp_async_commit();")
         e("    vt::cp_async_wait_group<0>();")
-        e(f"    vt::realign_row<NWC>(curA, llrA(0), (int)(oA0 & 15), "
-          f"(int)min(max((gA.s - gA.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
-        e(f"    vt::realign_row<NWC>(curB, llrB(0), (int)(oB0 & 15), "
-          f"(int)min(max((gB.s - gB.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B));")
+        zb0A = f"(int)min(max((gA.s - gA.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B)"
+        zb0B = f"(int)min(max((gB.s - gB.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B)"
+        if self.tc:
+            e("    {  // chunks 0 and 1 -> tiles 0 and 1 -> MMAs into TMEM buffers 0 and 1")
+            e("      uint32_t rA[NWC], rB[NWC];")
+            e(f"      vt::realign_row<NWC>(rA, llrA(0), (int)(oA0 & 15), {zb0A});")
+            e(f"      vt::realign_row<NWC>(rB, llrB(0), (int)(oB0 & 15), {zb0B});")
+            e("      tc_write(0, rA, rB);")
+            e("      if (a.nc > 1) {")
+            e("        vt::realign_row<NWC>(rA, llrA(1), (int)((oA + (int64_t)CH * B) & 15), "
+              "(int)min(max((gA.s - (gA.g0 + (int64_t)CH)) * B, (int64_t)0), (int64_t)CH * B));")
+            e("        vt::realign_row<NWC>(rB, llrB(1), (int)((oB + (int64_t)CH * B) & 15), "
+              "(int)min(max((gB.s - (gB.g0 + (int64_t)CH)) * B, (int64_t)0), (int64_t)CH * B));")
+            e("        tc_write(1, rA, rB);")
+            e("      }")
+            e("      tc_issue(0, a.nc > 1 ? 2 : 1);")
+            e("    }")
+        else:
+            e(f"    vt::realign_row<NWC>(curA, llrA(0), (int)(oA0 & 15), {zb0A});")
+            e(f"    vt::realign_row<NWC>(curB, llrB(0), (int)(oB0 & 15), {zb0B});")
         e(f"    int gidx = it0 * {self.GPB};")
         e("    // traceback of the previous tile: one group step per forward group, loads one group ahead")
         e("    for (int c = 0; c < a.nc; ++c) {")
@@ -446,10 +544,17 @@ class Gen16:
         e(f"        vt::stage_row<NL>(llrA(c & 1), a.llr, buf_bytes, onA + (int64_t)CH * B, fastA);")
         e(f"        vt::stage_row<NL>(llrB(c & 1), a.llr, buf_bytes, onB + (int64_t)CH * B, fastB);")
         e("      }")
-        if self.GPB % 2:
+        if self.GPB % 2 or self.tc:
+            # (tc: chunk c+2 is realigned at the end of THIS chunk, which may run no traceback
+            # step at all (leading-padding skip), so the staging needs its own commit group)
             e("      vt::cp_async_commit();")
         else:
             e("      // (no commit here: the staging rides on the next traceback step's commit group)")
+        if self.tc:
+            e("      vt::tc::mbar_wait(tc_bar + (c & 1), (tc_phase >> (c & 1)) & 1u);  // chunk c's branch metrics")
+            e("      tc_phase ^= 1u << (c & 1);")
+            e("      vt::tc::fence_after();")
+            e("      uint32_t tcA = tcrow + (uint32_t)(c & 1) * 128u;  // TMEM column of the next body's stage 0")
         e("#pragma unroll 1")
         e(f"      for (int it = it_start; it < {CH_BODIES}; ++it) {{")
         names = [f"m{j}" for j in range(S)]
@@ -464,21 +569,37 @@ class Gen16:
                     e(f"        m{j} = {names[j]};")
                 names = [f"m{j}" for j in range(S)]
                 self.group_end("        ", q // L)
-        self.shift_cur("        ")
+        if self.tc:
+            e(f"        tcA += {4 * P}u;")
+        else:
+            self.shift_cur("        ")
         e("      }")
         e("      it_start = 0;")
         e("      tbA.settle(a);  // whole words of the previous tile's traceback")
         e("      tbB.settle(a);")
-        e("      if (c + 1 < a.nc) {")
-        if self.GPB % 2:
-            e("        vt::cp_async_wait_group<1>();")
+        if self.tc:
+            e("      if (c + 2 < a.nc) {  // chunk c+2 -> tile (c & 1) -> MMA into TMEM buffer (c & 1)")
+            e("        if (c == 0) vt::cp_async_wait_group<0>(); else vt::cp_async_wait_group<3>();")
+            e("        uint32_t rA[NWC], rB[NWC];")
+            e("        const int64_t o2A = onA + (int64_t)CH * B, o2B = onB + (int64_t)CH * B;")
+            e("        vt::realign_row<NWC>(rA, llrA(c & 1), (int)(o2A & 15), "
+              "(int)min(max((gA.s - (gA.g0 + (int64_t)CH * (c + 2))) * B, (int64_t)0), (int64_t)CH * B));")
+            e("        vt::realign_row<NWC>(rB, llrB(c & 1), (int)(o2B & 15), "
+              "(int)min(max((gB.s - (gB.g0 + (int64_t)CH * (c + 2))) * B, (int64_t)0), (int64_t)CH * B));")
+            e("        tc_write(c & 1, rA, rB);")
+            e("        tc_issue(c & 1, 1);")
+            e("      }")
         else:
-            e(f"        vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 was committed >= 4 steps ago")
-        e(f"        vt::realign_row<NWC>(curA, llrA((c + 1) & 1), (int)(onA & 15), "
-          "(int)min(max((gA.s - (gA.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
-        e(f"        vt::realign_row<NWC>(curB, llrB((c + 1) & 1), (int)(onB & 15), "
-          "(int)min(max((gB.s - (gB.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
-        e("      }")
+            e("      if (c + 1 < a.nc) {")
+            if self.GPB % 2:
+                e("        vt::cp_async_wait_group<1>();")
+            else:
+                e(f"        vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 was committed >= 4 steps ago")
+            e(f"        vt::realign_row<NWC>(curA, llrA((c + 1) & 1), (int)(onA & 15), "
+              "(int)min(max((gA.s - (gA.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
+            e(f"        vt::realign_row<NWC>(curB, llrB((c + 1) & 1), (int)(onB & 15), "
+              "(int)min(max((gB.s - (gB.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
+            e("      }")
         e("    }")
         e("    // the previous tile's remaining traceback steps, then its unstored tail")
         if self.GPB % 2 == 0:
@@ -536,5 +657,9 @@ class Gen16:
             e("  while (tbB.running && tbB.b >= a.b_lo) tb_advance(tbB, nxtB, aftB, 16);")
         e("  if (tbA.running) tbA.drain_unstored(a);")
         e("  if (tbB.running) tbB.drain_unstored(a);")
+        if self.tc:
+            e("  vt::tc::fence_before();")
+            e("  __syncthreads();")
+            e("  if (tid < 32) vt::tc::dealloc<256>(tmb);")
         e("}")
         e("")

@@ -58,10 +58,11 @@ struct KernelEntry {
   const void* fn;
   const void* fn_nofm;  // variant without final-metric bookkeeping (nullptr: use fn)
   int smem;             // dynamic shared memory bytes per CTA
+  int tc;               // 1: tensor-core branch-metric variant (opt-in)
 };
 
-#define VT_KERNEL(fn_, fnnf_, smem_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, ...) \
-  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, __VA_ARGS__, (const void*)&fn_, (const void*)(fnnf_), smem_},
+#define VT_KERNEL(fn_, fnnf_, smem_, tc_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, ...) \
+  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, __VA_ARGS__, (const void*)&fn_, (const void*)(fnnf_), smem_, tc_},
 }  // namespace
 #include "gen/registry_decl.inc"
 namespace {
@@ -74,14 +75,21 @@ const KernelEntry* registry(int* n) {
   return table;
 }
 
-// Kernel variant: "16x2" (two windows per thread in packed 16-bit halves) or "s32" (one
-// window per thread, 32-bit metrics).  Default: 16x2 where it exists with >= 3-bit history
-// groups (K=7 rate 1/2: measured faster); s32 otherwise (K=7 rate 1/3 needs 2-bit groups,
-// whose group-end work makes the 16x2 form slower).  VT_KERNEL_VARIANT=16x2|s32 forces one.
-bool prefer16(const KernelEntry* e, const char* env) {
-  if (env && strcmp(env, "s32") == 0) return false;
-  if (env && strcmp(env, "16x2") == 0) return true;
-  return e->BL >= 3;
+// Kernel variant: "16x2" (two windows per thread in packed 16-bit halves), "s32" (one
+// window per thread, 32-bit metrics) or "16x2tc" (16x2 with the branch metrics of each
+// 12-stage chunk computed on the tensor cores: tcgen05 kind::i8, the paper's LLR x
+// codeword-matrix contraction).  Default: 16x2 where it exists with >= 3-bit history
+// groups (K=7 rate 1/2: measured fastest); s32 otherwise (K=7 rate 1/3 needs 2-bit
+// groups, whose group-end work makes the 16x2 form slower).  VT_KERNEL_VARIANT forces one.
+int variant_rank(const KernelEntry* e, const char* env) {
+  // lower is better; entries of the requested variant win, then the default order
+  const bool is16 = e->WPT > 1, istc = e->tc != 0;
+  if (env && strcmp(env, "16x2tc") == 0) return istc ? 0 : (is16 ? 1 : 2);
+  if (env && strcmp(env, "16x2") == 0) return (is16 && !istc) ? 0 : (istc ? 2 : 1);
+  if (env && strcmp(env, "s32") == 0) return is16 ? 2 : 0;
+  if (istc) return 3;                       // opt-in only
+  if (is16) return e->BL >= 3 ? 0 : 2;     // 16x2 preferred for >= 3-bit groups
+  return 1;
 }
 
 const KernelEntry* find(const vt_code* c) {
@@ -95,13 +103,7 @@ const KernelEntry* find(const vt_code* c) {
     bool same = true;
     for (int b = 0; b < c->B; ++b) same = same && t[i].gens[b] == c->gens[b];
     if (!same) continue;
-    if (!best) {
-      best = &t[i];
-    } else {  // two entries for this code: pick by variant
-      const KernelEntry* k16 = t[i].WPT > best->WPT ? &t[i] : best;
-      const KernelEntry* k32 = t[i].WPT > best->WPT ? best : &t[i];
-      best = prefer16(k16, env) ? k16 : k32;
-    }
+    if (!best || variant_rank(&t[i], env) < variant_rank(best, env)) best = &t[i];
   }
   return best;
 }
