@@ -120,12 +120,21 @@ class Gen16:
                 expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(self.B))
                 e(f"{ind}const uint32_t S{q}_{p} = {expr};")
             return
-        e(f"{ind}uint32_t ta{q}_0, ta{q}_1, ta{q}_2, ta{q}_3, tb{q}_0, tb{q}_1, tb{q}_2, tb{q}_3;")
-        e(f"{ind}vt::tc::ld4(tcA + {4 * q}u, ta{q}_0, ta{q}_1, ta{q}_2, ta{q}_3);")
-        e(f"{ind}vt::tc::ld4(tcA + {4 * q + self.TCN}u, tb{q}_0, tb{q}_1, tb{q}_2, tb{q}_3);")
+        # the loads of body stage q are issued during stage q-1 (stage 0 loads for itself),
+        # so tcgen05.wait::ld rarely waits
+        if q == 0:
+            self.tc_load(ind, 0)
         e(f"{ind}vt::tc::wait_ld();")
         for p in pats:  # window A in the low half, window B in the high half
             e(f"{ind}const uint32_t S{q}_{p} = vt::prmt(ta{q}_{p}, tb{q}_{p}, 0x5410u);")
+        if q + 1 < self.P:
+            self.tc_load(ind, q + 1)
+
+    def tc_load(self, ind: str, q: int) -> None:
+        e = self.emit
+        e(f"{ind}uint32_t ta{q}_0, ta{q}_1, ta{q}_2, ta{q}_3, tb{q}_0, tb{q}_1, tb{q}_2, tb{q}_3;")
+        e(f"{ind}vt::tc::ld4(tcA + {4 * q}u, ta{q}_0, ta{q}_1, ta{q}_2, ta{q}_3);")
+        e(f"{ind}vt::tc::ld4(tcA + {4 * q + self.TCN}u, tb{q}_0, tb{q}_1, tb{q}_2, tb{q}_3);")
 
     def stage(self, ind: str, q: int, names: list[str], defer: list | None = None) -> list[str]:
         """One radix-2 stage (body position q) for both windows.
