@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_metric_range.py tests/test_fileio.py -m gpu -q -x > gpurun_out/pytest.log 2>&1; echo "rc $?" >> gpurun_out/pytest.log
-timeout 300 python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-other-configs > gpurun_out/b.json 2>&1
-ncu --metrics gpu__time_duration.sum,sm__inst_executed.avg.per_cycle_active,smsp__average_warps_issue_stalled_wait_per_issue_active.ratio,smsp__inst_executed.sum --clock-control none -k regex:vtk16 -s 3 -c 1 --csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-other-configs > gpurun_out/ncu_q.csv 2>&1
+VT_KERNEL_VARIANT=16x2tc ncu --set full --clock-control none --import-source on -k regex:vtk16tc -s 3 -c 1 -f -o gpurun_out/prof_tc python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-other-configs > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/prof_tc.ncu-rep > gpurun_out/ncu_tc_summary.txt 2>&1
+ncu -i gpurun_out/prof_tc.ncu-rep --page source --csv --print-source sass > gpurun_out/tc_source.csv 2>/dev/null
+python tools/sass_hist.py gpurun_out/tc_source.csv --regions --stalls > gpurun_out/tc_sass_hist.txt 2>&1
