@@ -293,8 +293,16 @@ def other_configs(torch, vt, dev, steps: int) -> list:
              ("K=9 r1/2 (753,561) V=54", 9, (0o753, 0o561), 1 << 26, 256, 54)]
     for f in (64, 128, 256, 512, 1024):
         cases.append((f"K=7 r1/2 sweep F={f}", 7, GENS, 1 << 26, f, 42))
+    # the same headline code through the other kernel forms (VT_KERNEL_VARIANT)
+    cases.append(("K=7 r1/2 F=256 tensor-core branch metrics (16x2tc)", 7, GENS, 1 << 26, 256, 42, "16x2tc"))
+    cases.append(("K=7 r1/2 F=256 one window per thread (s32)", 7, GENS, 1 << 26, 256, 42, "s32"))
     stream = torch.cuda.current_stream()
-    for label, k, gens, n, f, v in cases:
+    for case in cases:
+        label, k, gens, n, f, v = case[:6]
+        variant = case[6] if len(case) > 6 else None
+        old_env = os.environ.get("VT_KERNEL_VARIANT")
+        if variant:
+            os.environ["VT_KERNEL_VARIANT"] = variant
         spec = vt.CodeSpec(k, gens)
         _, q = make_stream(torch, n, seed=77, device=dev, gens=gens, k=k)
         o = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev)
@@ -313,6 +321,11 @@ def other_configs(torch, vt, dev, steps: int) -> list:
         out.append({"config": label, "frame_len": f, "overlap": v, "stages": n, "windows": -(-n // f),
                     "value": round(n / (ms * 1e-3) / 1e9, 2), "unit": "Gbps", "ms_per_step": round(ms, 4),
                     "gstate_updates_per_s": round(su / (ms * 1e-3) / 1e9, 1)})
+        if variant:
+            if old_env is None:
+                os.environ.pop("VT_KERNEL_VARIANT", None)
+            else:
+                os.environ["VT_KERNEL_VARIANT"] = old_env
         del q, o
     return out
 
