@@ -14,7 +14,7 @@ want = oracle.decode_stream(q, 7, (0o171, 0o133), f, v, threads=8)
 print("mismatches", int(np.count_nonzero(got != want)))
 '''
 for n, f, v in [(1 << 18, 256, 42), (1 << 16, 256, 42), (65536 + 256 * 3, 256, 42), (4096, 256, 42), (60000, 256, 42)]:
-    env = dict(os.environ, VT_KERNEL_VARIANT="16x2tc")
+    env = dict(os.environ)
     try:
         r = subprocess.run([sys.executable, "-c", CODE, str(n), str(f), str(v)], env=env, capture_output=True,
                            text=True, timeout=40)
