@@ -35,6 +35,12 @@
  *   - Return 0 on success, a negative VT_E* code on error; vt_last_error()
  *     returns a message for the calling thread.
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Kernel form (same bits, different speed): the environment variable
+ *     VT_KERNEL_VARIANT = 16x2 | s32 | 16x2tc forces two windows per thread in
+ *     packed 16-bit halves, one window per thread with 32-bit metrics, or 16x2
+ *     with tensor-core (tcgen05 kind::i8) branch metrics; by default 16x2 is
+ *     used where it exists with 3-bit history groups (K=7 rate 1/2), s32
+ *     otherwise.
  */
 #ifndef VITERTILE_B200_H
 #define VITERTILE_B200_H

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-VT_KERNEL_VARIANT=16x2tc ncu --set full --clock-control none --import-source on -k regex:vtk16tc -s 3 -c 1 -f -o gpurun_out/prof_tc python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-other-configs > /dev/null 2>&1
-python tools/ncu_summary.py gpurun_out/prof_tc.ncu-rep > gpurun_out/ncu_tc_summary.txt 2>&1
-ncu -i gpurun_out/prof_tc.ncu-rep --page source --csv --print-source sass > gpurun_out/tc_source.csv 2>/dev/null
-python tools/sass_hist.py gpurun_out/tc_source.csv --regions --stalls > gpurun_out/tc_sass_hist.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_all.log 2>&1; echo "rc $?" >> gpurun_out/pytest_all.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_full.json 2>gpurun_out/bench_full.err
+bash tools/profile_round.sh > gpurun_out/profile_round.log 2>&1
