@@ -499,6 +499,10 @@ class Gen16:
         e("    // the window's whole staged span (16-byte words) lies inside the buffer: unchecked copies")
         e(f"    const int64_t span = (int64_t)a.nc * CH * B + 16 * NL;")
         e("    const bool fastA = oA >= 0 && oA + span <= buf_bytes, fastB = oB >= 0 && oB + span <= buf_bytes;")
+        e("    // 32-bit per-chunk bookkeeping: misalignment base and front-padding stages of each window")
+        e("    const int moA = (int)(oA & 15), moB = (int)(oB & 15);")
+        e(f"    const int padA = (int)min(max(gA.s - gA.g0, (int64_t)0), (int64_t){1 << 20}), "
+          f"padB = (int)min(max(gB.s - gB.g0, (int64_t)0), (int64_t){1 << 20});")
         m0 = (self.Sb << L) * 0x10001 if self.cheap else 0  # cheap stages need m_i1 + T >= 0 from the start
         e("    " + " ".join(f"uint32_t m{j} = {m0:#x}u;" for j in range(S)))
         e("    uint32_t negR = 0, negE = 0;")
@@ -550,8 +554,8 @@ class Gen16:
         e("    for (int c = 0; c < a.nc; ++c) {")
         e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
         e("      if (c + 2 < a.nc) {")
-        e(f"        vt::stage_row<NL>(llrA(c & 1), a.llr, buf_bytes, onA + (int64_t)CH * B, fastA);")
-        e(f"        vt::stage_row<NL>(llrB(c & 1), a.llr, buf_bytes, onB + (int64_t)CH * B, fastB);")
+        e(f"        vt::stage_row_rel<NL>(llrA(c & 1), a.llr, buf_bytes, oA, CH * B * (c + 2), fastA);")
+        e(f"        vt::stage_row_rel<NL>(llrB(c & 1), a.llr, buf_bytes, oB, CH * B * (c + 2), fastB);")
         e("      }")
         if self.GPB % 2 or self.tc:
             # (tc: chunk c+2 is realigned at the end of THIS chunk, which may run no traceback
@@ -604,10 +608,10 @@ class Gen16:
                 e("        vt::cp_async_wait_group<1>();")
             else:
                 e(f"        vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 was committed >= 4 steps ago")
-            e(f"        vt::realign_row<NWC>(curA, llrA((c + 1) & 1), (int)(onA & 15), "
-              "(int)min(max((gA.s - (gA.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
-            e(f"        vt::realign_row<NWC>(curB, llrB((c + 1) & 1), (int)(onB & 15), "
-              "(int)min(max((gB.s - (gB.g0 + (int64_t)CH * (c + 1))) * B, (int64_t)0), (int64_t)CH * B));")
+            e(f"        vt::realign_row<NWC>(curA, llrA((c + 1) & 1), (moA + CH * B * (c + 1)) & 15, "
+              "min(max((padA - CH * (c + 1)) * B, 0), CH * B));")
+            e(f"        vt::realign_row<NWC>(curB, llrB((c + 1) & 1), (moB + CH * B * (c + 1)) & 15, "
+              "min(max((padB - CH * (c + 1)) * B, 0), CH * B));")
             e("      }")
         e("    }")
         e("    // the previous tile's remaining traceback steps, then its unstored tail")

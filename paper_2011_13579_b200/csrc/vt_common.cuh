@@ -189,6 +189,20 @@ __device__ __forceinline__ void stage_row(char* row, const int8_t* __restrict__ 
   }
 }
 
+// stage_row at byte offset o = o0 + rel (rel 32-bit): the fast path needs no 64-bit
+// offset arithmetic beyond one pointer add
+template <int NL>
+__device__ __forceinline__ void stage_row_rel(char* row, const int8_t* __restrict__ llr, int64_t buf_bytes, int64_t o0,
+                                              int rel, bool fast) {
+  if (fast) {
+    const int8_t* p = reinterpret_cast<const int8_t*>(reinterpret_cast<uintptr_t>(llr + o0 + rel) & ~(uintptr_t)15);
+#pragma unroll
+    for (int i = 0; i < NL; ++i) cp_async16(row + 16 * i, p + 16 * i, 16, 0);
+  } else {
+    stage_row<NL>(row, llr, buf_bytes, o0 + rel, false);
+  }
+}
+
 // Words [o, o + 4*NWC) of a row staged by stage_row (off = o & 15): NWC+1 aligned
 // 4-byte loads and a funnel shift by the byte misalignment; zero the first zb bytes.
 template <int NWC>
