@@ -281,19 +281,18 @@ class Gen16:
         e(f"{ind}{{  // traceback step (previous tile, both windows)")
         e(f"{ind}  vt::cp_async_wait_group<{self.TBD - 1}>();")
         e(f"{ind}  const char* const rs = reinterpret_cast<const char*>(s_tb + tbr * {SQ * NT} + tid);")
-        e(f"{ind}  const uint32_t cA = tbA.j & {S - 8}u, cB = tbB.j & {S - 8}u;")
-        e(f"{ind}  const uint2 qa = *reinterpret_cast<const uint2*>(rs + (cA >> 4) * {NT * 16}u + (cA & 8u));")
-        e(f"{ind}  const uint2 qb = *reinterpret_cast<const uint2*>(rs + (cB >> 4) * {NT * 16}u + (cB & 8u));")
-        e(f"{ind}  const uint32_t lA = tbA.j & 7u, lB = tbB.j & 7u;")
-        e(f"{ind}  const uint32_t wA = (lA & 4u) ? qa.y : qa.x;")
-        e(f"{ind}  const uint32_t wB = (lB & 4u) ? qb.y : qb.x;")
-        e(f"{ind}  const uint32_t hA = (wA >> ({L}u * (lA & 3u))) & {fm}u;")
-        e(f"{ind}  const uint32_t hB = (wB >> (16u + {L}u * (lB & 3u))) & {fm}u;")
-        # unconditional: past the last stored group (or before the first traced tile) the
-        # walk runs on clamped junk, but those bits lie below every emit range and settle()
-        # writes nothing once a window is finished -- no branch splits the ACS block
-        e(f"{ind}  tbA.step(hA);")
-        e(f"{ind}  tbB.step(hB);")
+        # state j's 3-bit field: word j >> 2 of the group (uint4 j >> 4, word (j >> 2) & 3),
+        # bit offset 3 * (j & 3) (+16 for window B)
+        for w, side in (("A", 0), ("B", 16)):
+            e(f"{ind}  {{")
+            e(f"{ind}    const uint32_t j = tb{w}.j;")
+            e(f"{ind}    const uint32_t wd = *reinterpret_cast<const uint32_t*>(rs + ((j & 48u) << 7) + (j & 12u));")
+            e(f"{ind}    const uint32_t h = (wd >> ((j & 3u) * {L}u + {side}u)) & {fm}u;")
+            e(f"{ind}    tb{w}.acc = (tb{w}.acc << {L}) | (j >> {self.k - L});")
+            e(f"{ind}    tb{w}.j = ((j << {L}) | h) & {S - 1}u;")
+            e(f"{ind}    tb{w}.lo -= {L};")
+            e(f"{ind}    --tb{w}.b;")
+            e(f"{ind}  }}")
         e(f"{ind}  --tbb;")
         self.tb_fetch(ind + "  ", f"tbb - {self.TBD - 1}", "tbr")
         e(f"{ind}  tbr = (tbr + 1) & {self.TBD - 1};")
