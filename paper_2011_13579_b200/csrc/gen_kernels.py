@@ -367,7 +367,7 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
     os.makedirs(outdir, exist_ok=True)
     files = []
     reg = ["// GENERATED by gen_kernels.py -- kernel registry:",
-           "// VT_KERNEL(fn, fn without final metrics or nullptr, dynamic smem bytes, tensor-core BM, K, B, lanes/window T, windows/thread, SL, chunk CH, history group BL, uint4/group SQ, {gens})",
+           "// VT_KERNEL(fn, fn without final metrics or nullptr, dynamic smem bytes, tensor-core BM, threads per CTA, K, B, lanes/window T, windows/thread, SL, chunk CH, history group BL, uint4/group SQ, {gens})",
            ""]
     decl = ["// GENERATED by gen_kernels.py -- kernel declarations", '#include "../vt_common.cuh"', ""]
     for name, (K, polys) in codes.items():
@@ -382,7 +382,7 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
         files.append(path)
         gl = ", ".join(f"{x}u" for x in gens)
         decl.append(f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);')
-        reg.append(f"VT_KERNEL(vtk_{name}, nullptr, 0, 0, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, {g.SQ}, {{{gl}}})")
+        reg.append(f"VT_KERNEL(vtk_{name}, nullptr, 0, 0, {NT}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, {g.SQ}, {{{gl}}})")
         if K == 7:  # packed 16x2 variant: two windows per thread
             import sys
             here = os.path.dirname(os.path.abspath(__file__))
@@ -398,7 +398,8 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
             files.append(path16)
             decl.append(f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a);')
             decl.append(f'extern "C" __global__ void vtk16nf_{name}(const vt::StreamArgs a);')
-            if g16.cheap:  # tensor-core branch-metric variant (VT_KERNEL_VARIANT=16x2tc)
+            import gen_kernels16
+            if g16.cheap and gen_kernels16.NT == 128:  # tensor-core branch-metric variant (VT_KERNEL_VARIANT=16x2tc)
                 gtc = Gen16(name, K, gens, tc=True)
                 srctc = gtc.kernel()
                 pathtc = os.path.join(outdir, f"vtk16tc_{name}.cu")
@@ -408,9 +409,10 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
                 files.append(pathtc)
                 decl.append(f'extern "C" __global__ void vtk16tc_{name}(const vt::StreamArgs a);')
                 decl.append(f'extern "C" __global__ void vtk16tcnf_{name}(const vt::StreamArgs a);')
-                reg.append(f"VT_KERNEL(vtk16tc_{name}, &vtk16tcnf_{name}, {gtc.SMEM}, 1, {K}, {len(gens)}, 1, 2, "
+                reg.append(f"VT_KERNEL(vtk16tc_{name}, &vtk16tcnf_{name}, {gtc.SMEM}, 1, 128, {K}, {len(gens)}, 1, 2, "
                            f"{gtc.S}, {gtc.CH}, {gtc.L}, {gtc.S // 16}, {{{gl}}})")
-            reg.append(f"VT_KERNEL(vtk16_{name}, &vtk16nf_{name}, {g16.SMEM}, 0, {K}, {len(gens)}, 1, 2, {g16.S}, {g16.CH}, {g16.L}, "
+            import gen_kernels16
+            reg.append(f"VT_KERNEL(vtk16_{name}, &vtk16nf_{name}, {g16.SMEM}, 0, {gen_kernels16.NT}, {K}, {len(gens)}, 1, 2, {g16.S}, {g16.CH}, {g16.L}, "
                        f"{g16.S // 16}, {{{gl}}})")
     for fname, lines in (("registry.inc", reg), ("registry_decl.inc", decl)):
         rpath = os.path.join(outdir, fname)

@@ -26,7 +26,11 @@ walks groups: j_prev = ((j << L) | h) & (S-1), decoded bits =
 """
 from __future__ import annotations
 
-from gen_kernels import NT, parity
+import os
+
+from gen_kernels import parity
+
+NT = int(os.environ.get("VT_NT16", "128"))  # threads per CTA of the 16x2 kernels (2 windows each)
 
 CH_BODIES = 2  # loop bodies per LLR chunk
 MINB16 = 1  # CTAs per SM bound (3 forces a 168-register cap: spills, measured 16% slower with the ring traceback)

@@ -26,7 +26,7 @@ int cuda_fail(cudaError_t e, const char* what) {
   return fail(VT_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-constexpr int kNT = 128;  // threads (= windows) per CTA
+// (threads per CTA: KernelEntry::nt)
 
 struct Geometry {
   int64_t nwin;
@@ -59,10 +59,11 @@ struct KernelEntry {
   const void* fn_nofm;  // variant without final-metric bookkeeping (nullptr: use fn)
   int smem;             // dynamic shared memory bytes per CTA
   int tc;               // 1: tensor-core branch-metric variant (opt-in)
+  int nt;               // threads per CTA
 };
 
-#define VT_KERNEL(fn_, fnnf_, smem_, tc_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, ...) \
-  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, __VA_ARGS__, (const void*)&fn_, (const void*)(fnnf_), smem_, tc_},
+#define VT_KERNEL(fn_, fnnf_, smem_, tc_, nt_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, ...) \
+  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, __VA_ARGS__, (const void*)&fn_, (const void*)(fnnf_), smem_, tc_, nt_},
 }  // namespace
 #include "gen/registry_decl.inc"
 namespace {
@@ -136,19 +137,19 @@ int ctas_per_sm(const KernelEntry* k) {
   if (env && atoi(env) > 0) return atoi(env);
   prepare(k);
   int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, kNT, k->smem) != cudaSuccess || occ < 1) occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->nt, k->smem) != cudaSuccess || occ < 1) occ = 1;
   return std::min(occ, 4);
 }
 
 int64_t grid_for(const KernelEntry* k, int64_t nwin) {
-  const int64_t wpc = (int64_t)kNT * k->WPT / k->T;  // windows per CTA
+  const int64_t wpc = (int64_t)k->nt * k->WPT / k->T;  // windows per CTA
   const int64_t tiles = (nwin + wpc - 1) / wpc;
   const int64_t cap = (int64_t)device_sms() * ctas_per_sm(k);
   return std::max<int64_t>(1, std::min(tiles, cap));
 }
 
 size_t scratch_bytes(const KernelEntry* k, const Geometry& g, int64_t grid) {
-  return (size_t)grid * g.nbs * k->SQ * kNT * sizeof(uint4);
+  return (size_t)grid * g.nbs * k->SQ * k->nt * sizeof(uint4);
 }
 
 }  // namespace
@@ -217,7 +218,7 @@ int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, 
   void* args[] = {&a};
   const void* fn = (final_metric == nullptr && k->fn_nofm) ? k->fn_nofm : k->fn;
   prepare(k);
-  cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kNT), args, (size_t)k->smem, (cudaStream_t)stream);
+  cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(k->nt), args, (size_t)k->smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return VT_OK;
 }
