@@ -72,7 +72,12 @@ class Gen16:
         self.B = len(gens)
         self.L = history_bits(K, self.B)
         self.P = self.k  # body length: the state->register naming returns to the identity
-        self.CH = self.P * CH_BODIES  # LLR chunk (stages)
+        self.GPB = self.P // self.L  # history groups per body
+        # per-body LLR realignment from the staged rows (4-body chunks: half the per-chunk
+        # bookkeeping per group, 3 LLR words per window in registers instead of 6)
+        self.pbr = (not tc) and self.GPB % 2 == 0
+        self.CHB = int(os.environ.get("VT_CHB16", "4")) if self.pbr else CH_BODIES
+        self.CH = self.P * self.CHB  # LLR chunk (stages)
         self.GPB = self.P // self.L  # history groups per body
         self.dmax = 128 * self.B
         self.Sb = 2 * self.k * self.dmax
@@ -95,6 +100,9 @@ class Gen16:
         self.NL = -(-(self.NWC * 4 + 15) // 16)
         while self.NWC + 4 > 4 * self.NL:
             self.NL += 1
+        self.NWB = -(-self.P * self.B // 4)  # LLR words per body (per-body realignment)
+        if self.pbr:  # a body's words start anywhere in the row: 15 + CH*B bytes + one word of lookahead
+            self.NL = -(-(15 + self.CH * self.B + 4) // 16)
         self.lines: list[str] = []
         ring = self.TBD * (self.S // 16) if self.GPB % 2 == 0 else 0
         self.SMEM = (4 * self.NL + ring) * NT * 16  # dynamic shared memory bytes
@@ -512,20 +520,26 @@ class Gen16:
         if self.fm:
             o0 = -self.Sb if self.cheap else 0
             e(f"    int64_t offA = {o0}, offB = {o0}, pendA = 0, pendB = 0;")
-        if not self.tc:
+        if self.pbr:
+            e(f"    uint32_t curA[{self.NWB}], curB[{self.NWB}];  // this body's LLR words (realigned per body)")
+        elif not self.tc:
             e("    uint32_t curA[NWC], curB[NWC];")
         e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole bodies of it")
         if self.tc:  # warp-uniform: tcgen05.ld is .sync.aligned, so every lane must run the same bodies
             e(f"    const int it0 = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)min(min(max(gA.s - gA.g0, (int64_t)0), "
-              f"max(gB.s - gB.g0, (int64_t)0)) / {P}, (int64_t){CH_BODIES}));")
+              f"max(gB.s - gB.g0, (int64_t)0)) / {P}, (int64_t){self.CHB}));")
         else:
             e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
-              f"(int64_t){CH_BODIES});")
+              f"(int64_t){self.CHB});")
         e("    int it_start = it0;")
         e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
         e("    // chunks are staged two ahead (cp.async groups): chunk k lives in buffer k & 1")
-        e(f"    vt::stage_row<NL>(llrA(0), a.llr, buf_bytes, oA0, fastA);")
-        e(f"    vt::stage_row<NL>(llrB(0), a.llr, buf_bytes, oB0, fastB);")
+        if self.pbr:
+            e(f"    vt::stage_row<NL>(llrA(0), a.llr, buf_bytes, oA, fastA);")
+            e(f"    vt::stage_row<NL>(llrB(0), a.llr, buf_bytes, oB, fastB);")
+        else:
+            e(f"    vt::stage_row<NL>(llrA(0), a.llr, buf_bytes, oA0, fastA);")
+            e(f"    vt::stage_row<NL>(llrB(0), a.llr, buf_bytes, oB0, fastB);")
         e("    if (a.nc > 1) {")
         e(f"      vt::stage_row<NL>(llrA(1), a.llr, buf_bytes, oA + (int64_t)CH * B, fastA);")
         e(f"      vt::stage_row<NL>(llrB(1), a.llr, buf_bytes, oB + (int64_t)CH * B, fastB);")
@@ -549,22 +563,23 @@ class Gen16:
             e("      }")
             e("      tc_issue(0, a.nc > 1 ? 2 : 1);")
             e("    }")
-        else:
+        elif not self.pbr:
             e(f"    vt::realign_row<NWC>(curA, llrA(0), (int)(oA0 & 15), {zb0A});")
             e(f"    vt::realign_row<NWC>(curB, llrB(0), (int)(oB0 & 15), {zb0B});")
         e(f"    int gidx = it0 * {self.GPB};")
         e("    // traceback of the previous tile: one group step per forward group, loads one group ahead")
         e("    for (int c = 0; c < a.nc; ++c) {")
         e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
-        e("      if (c + 2 < a.nc) {")
-        e(f"        vt::stage_row_rel<NL>(llrA(c & 1), a.llr, buf_bytes, oA, CH * B * (c + 2), fastA);")
-        e(f"        vt::stage_row_rel<NL>(llrB(c & 1), a.llr, buf_bytes, oB, CH * B * (c + 2), fastB);")
-        e("      }")
+        if not self.pbr:
+            e("      if (c + 2 < a.nc) {")
+            e(f"        vt::stage_row_rel<NL>(llrA(c & 1), a.llr, buf_bytes, oA, CH * B * (c + 2), fastA);")
+            e(f"        vt::stage_row_rel<NL>(llrB(c & 1), a.llr, buf_bytes, oB, CH * B * (c + 2), fastB);")
+            e("      }")
         if self.GPB % 2 or self.tc:
             # (tc: chunk c+2 is realigned at the end of THIS chunk, which may run no traceback
             # step at all (leading-padding skip), so the staging needs its own commit group)
             e("      vt::cp_async_commit();")
-        else:
+        elif not self.pbr:
             e("      // (no commit here: the staging rides on the next traceback step's commit group)")
         if self.tc:
             e("      vt::tc::mbar_wait(tc_bar + (c & 1), (tc_phase >> (c & 1)) & 1u);  // chunk c's branch metrics")
@@ -572,7 +587,12 @@ class Gen16:
             e("      vt::tc::fence_after();")
             e("      uint32_t tcA = tcrow + (uint32_t)(c & 1) * 128u;  // TMEM column of the next body's stage 0")
         e("#pragma unroll 1")
-        e(f"      for (int it = it_start; it < {CH_BODIES}; ++it) {{")
+        e(f"      for (int it = it_start; it < {self.CHB}; ++it) {{")
+        if self.pbr:
+            e("        // this body's LLR words straight from the staged row of chunk c")
+            for w in ("A", "B"):
+                e(f"        vt::realign_row_at<{self.NWB}>(cur{w}, llr{w}(c & 1), ((mo{w} + CH * B * c) & 15) + {P * B} * it, "
+                  f"min(max((pad{w} - CH * c - {P} * it) * B, 0), {P * B}));")
         names = [f"m{j}" for j in range(S)]
         deferred: list = []
         for q in range(P):
@@ -587,7 +607,7 @@ class Gen16:
                 self.group_end("        ", q // L)
         if self.tc:
             e(f"        tcA += {4 * P}u;")
-        else:
+        elif not self.pbr:
             self.shift_cur("        ")
         e("      }")
         e("      it_start = 0;")
@@ -605,6 +625,14 @@ class Gen16:
             e("        tc_write(c & 1, rA, rB);")
             e("        tc_issue(c & 1, 1);")
             e("      }")
+        elif self.pbr:
+            e("      // chunk c's rows are consumed: stage chunk c+2 into its buffer (rides on the next")
+            e("      // traceback step's commit group, >= 4 steps before chunk c+2 starts)")
+            e("      if (c + 2 < a.nc) {")
+            e(f"        vt::stage_row_rel<NL>(llrA(c & 1), a.llr, buf_bytes, oA, CH * B * (c + 2), fastA);")
+            e(f"        vt::stage_row_rel<NL>(llrB(c & 1), a.llr, buf_bytes, oB, CH * B * (c + 2), fastB);")
+            e("      }")
+            e(f"      if (c + 1 < a.nc) vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 landed")
         else:
             e("      if (c + 1 < a.nc) {")
             if self.GPB % 2:

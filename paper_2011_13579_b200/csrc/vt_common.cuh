@@ -203,6 +203,27 @@ __device__ __forceinline__ void stage_row_rel(char* row, const int8_t* __restric
   }
 }
 
+// NWB words starting at byte `off` (any alignment) of a staged row: NWB+1 aligned 4-byte
+// loads and a funnel shift; zero the first zb bytes (stages before the window start)
+template <int NWB>
+__device__ __forceinline__ void realign_row_at(uint32_t (&out)[NWB], const char* row, int off, int zb) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row + (off & ~3));
+  uint32_t v[NWB + 1];
+#pragma unroll
+  for (int k = 0; k <= NWB; ++k) v[k] = w[k];
+  const int r = (off & 3) * 8;
+#pragma unroll
+  for (int k = 0; k < NWB; ++k) out[k] = __funnelshift_r(v[k], v[k + 1], r);
+  if (zb > 0) {
+#pragma unroll
+    for (int k = 0; k < NWB; ++k) {
+      const int lo = zb - 4 * k;
+      if (lo >= 4) out[k] = 0u;
+      else if (lo > 0) out[k] &= 0xFFFFFFFFu << (8 * lo);
+    }
+  }
+}
+
 // Words [o, o + 4*NWC) of a row staged by stage_row (off = o & 15): NWC+1 aligned
 // 4-byte loads and a funnel shift by the byte misalignment; zero the first zb bytes.
 template <int NWC>
