@@ -399,7 +399,7 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
             decl.append(f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a);')
             decl.append(f'extern "C" __global__ void vtk16nf_{name}(const vt::StreamArgs a);')
             import gen_kernels16
-            if g16.cheap and gen_kernels16.NT == 128:  # tensor-core branch-metric variant (VT_KERNEL_VARIANT=16x2tc)
+            if g16.cheap and g16.B == 2 and gen_kernels16.NT == 128:  # tensor-core branch-metric variant (VT_KERNEL_VARIANT=16x2tc)
                 gtc = Gen16(name, K, gens, tc=True)
                 srctc = gtc.kernel()
                 pathtc = os.path.join(outdir, f"vtk16tc_{name}.cu")

@@ -15,10 +15,11 @@ Per 16-bit half:  U = Lambda * 2^L + h  (unsigned), where
     the reference tie rule take1 = cand1 >= cand0, reference.py:121);
   * Lambda is the biased path metric: every LLR term enters as l+128 or 128-l
     (both >= 0), so each stage adds delta + 128*B >= 0; at each group start the
-    metrics are renormalised by Lambda_0 - S_b (S_b = 2(K-1)*128*B bounds the
-    metric spread), keeping Lambda in [0, 2*S_b + L*256*B] < 2^(16-L) (L = 3 for
-    K=7 r1/2, 2 for K=7 r1/3).  Per-half arithmetic is modular; the true values
-    stay in range, so the unsigned max is exact.
+    metrics are renormalised by Lambda_0 - S_b (S_b bounds the metric spread),
+    keeping Lambda in [0, 2*S_b + L*256*B] < 2^(16-L) (L = 3 for K=7 r1/2); K=7
+    r1/3 renormalises by the exact per-half minimum instead (Gen16.xmin), which
+    halves the span and also fits L = 3.  Per-half arithmetic is modular; the
+    true values stay in range, so the unsigned max is exact.
 At each group end the L-bit fields are masked out, packed 4 states per word
 (12 bits per half), streamed to the scratch slot and cleared.  The traceback
 walks groups: j_prev = ((j << L) | h) & (S-1), decoded bits =
@@ -70,7 +71,18 @@ class Gen16:
         assert self.S >= 16, "16x2 kernels pack 16 states per uint4 of history words"
         self.gens = gens
         self.B = len(gens)
-        self.L = history_bits(K, self.B)
+        self.dmax = 128 * self.B
+        delta = 256 * spread_weight(K, gens)
+        # Exact-minimum renormalisation (xmin): when renormalising by state 0 forces
+        # history groups narrower than 3 bits (K=7 r1/3), renormalise by the exact
+        # per-half minimum over the 2^(K-1) states instead (~S/2 VIMNMX3.U16x2 per
+        # group): the metrics then span [Sb', Sb' + Delta] at a group start instead of
+        # [Sb - Delta, Sb + Delta], which fits 3-bit groups.
+        L = history_bits(K, self.B)
+        self.xmin = False
+        if L < 3 and self.k % 3 == 0 and delta + 3 * 2 * self.dmax < (1 << 13):
+            L, self.xmin = 3, True
+        self.L = L
         self.P = self.k  # body length: the state->register naming returns to the identity
         self.GPB = self.P // self.L  # history groups per body
         # per-body LLR realignment from the staged rows (4-body chunks: half the per-chunk
@@ -79,7 +91,6 @@ class Gen16:
         self.CHB = int(os.environ.get("VT_CHB16", "6")) if self.pbr else CH_BODIES  # 6: measured best (4: -1%, 8: -13%)
         self.CH = self.P * self.CHB  # LLR chunk (stages)
         self.GPB = self.P // self.L  # history groups per body
-        self.dmax = 128 * self.B
         self.Sb = 2 * self.k * self.dmax
         # Cheap middle stage (see stage()): needs 3-bit groups, an even number of groups
         # per body and complementary branch patterns of the two predecessors (every
@@ -90,11 +101,14 @@ class Gen16:
         comp = all(self.pattern(((j << 1) & (self.S - 1)) | 1, j >> (self.k - 1)) ==
                    self.pattern((j << 1) & (self.S - 1), j >> (self.k - 1)) ^ ((1 << self.B) - 1)
                    for j in range(self.S))
-        delta = 256 * spread_weight(K, gens)
         sbc = delta + 2 * self.dmax
-        self.cheap = (self.L == 3 and self.GPB % 2 == 0 and comp and
+        # (not with xmin: for B = 3 the offset stage needs 64 + 64 combo adds per group,
+        # measured slower than the plain stage: 98.5 vs 100.5 Gbps for K=7 r1/3)
+        self.cheap = (not self.xmin and self.L == 3 and self.GPB % 2 == 0 and comp and
                       sbc + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)))
-        if self.cheap:
+        if self.xmin:  # the minimum renormalises to 0
+            self.Sb = 0
+        elif self.cheap:
             self.Sb = sbc
         self.NWC = -(-self.CH * self.B // 4)
         self.NL = -(-(self.NWC * 4 + 15) // 16)
@@ -324,7 +338,21 @@ class Gen16:
             e(f"{ind}offA += pendA;")
             e(f"{ind}offB += pendB;")
         e(f"{ind}{{")
-        e(f"{ind}  const uint32_t r0 = m0 & {lm:#x}u;")
+        if self.xmin:  # exact per-half minimum over all states (history bits masked after)
+            vals = [f"m{j}" for j in range(S)]
+            lvl = 0
+            while len(vals) > 1:
+                nxt = []
+                for i in range(0, len(vals) - 1, 2):
+                    nm = f"mn{lvl}_{i // 2}"
+                    e(f"{ind}  const uint32_t {nm} = vt::vmin2({vals[i]}, {vals[i + 1]});")
+                    nxt.append(nm)
+                if len(vals) % 2:
+                    nxt.append(vals[-1])
+                vals, lvl = nxt, lvl + 1
+            e(f"{ind}  const uint32_t r0 = {vals[0]} & {lm:#x}u;")
+        else:
+            e(f"{ind}  const uint32_t r0 = m0 & {lm:#x}u;")
         e(f"{ind}  const uint32_t rr = vt::vadd2(r0, {((-(self.Sb << L)) & 0xFFFF) * 0x10001:#x}u);")
         e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);  // -R per half, mod 2^16 (fused-add operand)")
         e(f"{ind}  negE = {(self.Sb << L) * 0x10001:#x}u - r0;  // -R as a packed integer (IMAD operand)")

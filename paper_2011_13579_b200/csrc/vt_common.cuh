@@ -52,6 +52,12 @@ __device__ __forceinline__ uint32_t vadd2(uint32_t a, uint32_t b) {
   asm("add.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
 }
+// per-half unsigned min (ptxas fuses pairs into VIMNMX3.U16x2)
+__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
 __device__ __forceinline__ uint32_t vaddmax2(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("{.reg .b32 t; add.u16x2 t, %1, %2; max.u16x2 %0, t, %3;}" : "=r"(d) : "r"(a), "r"(b), "r"(c));

@@ -1,24 +1,32 @@
 """Adversarial LLR stream for the 16-bit metric range of the 16x2 kernels.
 
-Greedy search over max-magnitude LLR pairs that maximises the K=7 (171,133)
-path-metric spread after each stage (2-step lookahead, random tie-breaks).  The
-16x2 kernels' range argument needs spread <= 256 * W6 = 2816 (W6 = 11, the
-code's maximum output-difference weight over 6 stages); this stream reaches
-2048.  Output: tests/golden/adversarial_k7r2.npz (int8 (N, 2)).
+Greedy search over max-magnitude LLR tuples that maximises the K=7 path-metric
+spread after each stage (2-step lookahead, random tie-breaks).  The 16x2
+kernels' range argument needs spread <= 256 * W6 (W6 = the code's maximum
+output-difference weight over 6 stages: 11 for (171,133), 15 for the r1/3
+(133,171,165)).  (171,133) reaches 2048 of 2816.
+usage: python make_adversarial.py [k7r2|k7r3]
+Output: tests/golden/adversarial_<code>.npz (int8 (N, B)).
 """
-import numpy as np, sys
-sys.path.insert(0, "/root/repo")
-K=7; G=(0o171,0o133); S=64
+import itertools, numpy as np, sys
+CODES={"k7r2": (0o171,0o133), "k7r3": (0o133,0o171,0o165)}
+name=sys.argv[1] if len(sys.argv)>1 else "k7r2"
+K=7; G=CODES[name]; S=64
 def parity(x): return bin(x).count("1")&1
 pred0=np.array([(2*(j%32)) for j in range(S)]); pred1=pred0+1
 def pat(i,u): reg=(u<<6)|i; return [1-2*parity(g&reg) for g in G]
 sg0=np.array([pat(pred0[j], j>>5) for j in range(S)]); sg1=np.array([pat(pred1[j], j>>5) for j in range(S)])
-cands=[np.array(c) for c in [(127,127),(127,-128),(-128,127),(-128,-128),(0,0),(127,0),(0,127),(-128,0),(0,-128)]]
+if name=="k7r2":
+    cands=[np.array(c) for c in [(127,127),(127,-128),(-128,127),(-128,-128),(0,0),(127,0),(0,127),(-128,0),(0,-128)]]
+else:  # max-magnitude corners first (the 2-step lookahead scans cands[:4])
+    corners=[np.array(c) for c in itertools.product((127,-128), repeat=len(G))]
+    cands=corners+[np.array(c) for c in itertools.product((127,-128,0), repeat=len(G)) if 0 in c]
+trials=40 if name=="k7r2" else 20
 def step(M,l):
     return np.maximum(M[pred0]+sg0@l, M[pred1]+sg1@l)
 rng=np.random.default_rng(0)
 best_overall=0; seqs=[]
-for trial in range(40):
+for trial in range(trials):
     M=np.zeros(S,np.int64); seq=[]
     for t in range(600):
         # greedy with random tie-break + 2-step lookahead on a random subset
@@ -31,6 +39,7 @@ for trial in range(40):
         M=step(M,c); M-=M.max(); seq.append(c)
         best_overall=max(best_overall, -M.min())
     seqs.append(np.array(seq))
-print("max spread observed", best_overall, "bound", 256*11)
+W={"k7r2":11,"k7r3":15}[name]
+print("max spread observed", best_overall, "bound", 256*W)
 import os
-np.savez_compressed(os.path.join(os.path.dirname(os.path.abspath(__file__)), "adversarial_k7r2.npz"), llr=np.concatenate(seqs).astype(np.int8), max_spread=np.int64(best_overall))
+np.savez_compressed(os.path.join(os.path.dirname(os.path.abspath(__file__)), f"adversarial_{name}.npz"), llr=np.concatenate(seqs).astype(np.int8), max_spread=np.int64(best_overall))

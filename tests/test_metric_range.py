@@ -1,7 +1,9 @@
 """The 16x2 kernels keep path metrics in 16-bit halves; their range argument
-(gen_kernels16.py) bounds the K=7 (171,133) metric spread by 256 * W6 with W6
-the code's maximum output-difference weight over 6 stages.  CPU: the bound's
-inputs and an adversarial stream's spread; GPU: that stream decodes exactly."""
+(gen_kernels16.py) bounds the K=7 metric spread by 256 * W6, W6 the code's
+maximum output-difference weight over 6 stages.  (171,133) renormalises by
+state 0 (span 2*Delta), the r1/3 (133,171,165) by the exact minimum (span
+Delta).  CPU: the bound's inputs and adversarial streams' spreads; GPU: those
+streams decode exactly."""
 import os
 
 import numpy as np
@@ -10,11 +12,15 @@ import pytest
 from conftest import ROOT
 from oracle import oracle
 
-ADV = os.path.join(ROOT, "tests", "golden", "adversarial_k7r2.npz")
-K, GENS = 7, (0o171, 0o133)
+CODES = {"k7r2": ((0o171, 0o133), 11, 1500), "k7r3": ((0o133, 0o171, 0o165), 15, 2500)}
+K = 7
 
 
-def _spread_weight():
+def _adv(name):
+    return os.path.join(ROOT, "tests", "golden", f"adversarial_{name}.npz")
+
+
+def _gen16():
     import sys
     sys.path.insert(0, os.path.join(ROOT, "paper_2011_13579_b200", "csrc"))
     from gen_kernels16 import Gen16, spread_weight
@@ -22,41 +28,61 @@ def _spread_weight():
 
 
 def test_spread_bound_inputs():
-    spread_weight, Gen16 = _spread_weight()
-    assert spread_weight(7, GENS) == 11
-    g = Gen16("k7r2", 7, GENS)
-    assert g.cheap and g.L == 3 and g.Sb == 256 * 11 + 512
+    spread_weight, Gen16 = _gen16()
+    gens, w6, _ = CODES["k7r2"]
+    assert spread_weight(7, gens) == w6
+    g = Gen16("k7r2", 7, gens)
+    assert g.cheap and not g.xmin and g.L == 3 and g.Sb == 256 * w6 + 512
     # Lambda stays below 2^13 inside a group: Sb' + Delta + 3 stages of growth
-    assert g.Sb + 256 * 11 + 3 * 512 < (1 << 13)
+    assert g.Sb + 256 * w6 + 3 * 512 < (1 << 13)
 
 
-def test_adversarial_stream_spread_within_bound():
-    q = np.load(ADV)["llr"].astype(np.int64)
+def test_spread_bound_inputs_r13_exact_min():
+    spread_weight, Gen16 = _gen16()
+    gens, w6, _ = CODES["k7r3"]
+    assert spread_weight(7, gens) == w6
+    g = Gen16("k7r3", 7, gens)
+    # renormalising by state 0 would need 2*Delta + 3*768 < 2^13 (false); by the exact
+    # minimum (to 0), Delta + 3 stages of growth fits 3-bit groups
+    assert 2 * 256 * w6 + 3 * 768 >= (1 << 13)
+    assert g.xmin and not g.cheap and g.L == 3 and g.Sb == 0
+    assert 256 * w6 + 3 * 768 < (1 << 13)
+
+
+@pytest.mark.parametrize("name", sorted(CODES))
+def test_adversarial_stream_spread_within_bound(name):
+    gens, w6, floor = CODES[name]
+    q = np.load(_adv(name))["llr"].astype(np.int64)
+    assert q.shape[1] == len(gens)
     S = 64
 
     def par(x):
         return bin(x).count("1") & 1
     p0 = np.array([2 * (j % 32) for j in range(S)])
-    sg0 = np.array([[1 - 2 * par(g & ((j >> 5) << 6 | p0[j])) for g in GENS] for j in range(S)])
-    sg1 = np.array([[1 - 2 * par(g & ((j >> 5) << 6 | (p0[j] + 1))) for g in GENS] for j in range(S)])
+    sg0 = np.array([[1 - 2 * par(g & ((j >> 5) << 6 | p0[j])) for g in gens] for j in range(S)])
+    sg1 = np.array([[1 - 2 * par(g & ((j >> 5) << 6 | (p0[j] + 1))) for g in gens] for j in range(S)])
     m = np.zeros(S, np.int64)
     worst = 0
     for t in range(q.shape[0]):
         m = np.maximum(m[p0] + sg0 @ q[t], m[p0 + 1] + sg1 @ q[t])
         m -= m.max()
         worst = max(worst, -int(m.min()))
-    assert worst <= 256 * 11
-    assert worst >= 1500  # the stream really is adversarial (regenerate with make_adversarial.py)
+    assert worst <= 256 * w6
+    assert worst >= floor  # the stream really is adversarial (regenerate with make_adversarial.py)
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["16x2", "s32"])
+@pytest.mark.parametrize("name", sorted(CODES))
 @pytest.mark.parametrize("fv", [(256, 42), (1000, 60), (31, 7), (24000, 0)])
-def test_adversarial_stream_decodes_exactly(fv):
+def test_adversarial_stream_decodes_exactly(name, fv, variant, monkeypatch):
     import paper_2011_13579_b200 as vt
     import torch
-    q = np.load(ADV)["llr"]
+    monkeypatch.setenv("VT_KERNEL_VARIANT", variant)
+    gens = CODES[name][0]
+    q = np.load(_adv(name))["llr"]
     f, v = fv
-    want = oracle.decode_stream(q, K, GENS, f, v, threads=8)
-    out = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(K, GENS), f, v)
+    want = oracle.decode_stream(q, K, gens, f, v, threads=8)
+    out = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(K, gens), f, v)
     got = np.unpackbits(out.cpu().numpy().view(np.uint8), count=q.shape[0], bitorder="little")
     np.testing.assert_array_equal(got, want)
