@@ -162,10 +162,18 @@ def run_ours(args) -> None:
     import paper_2011_13579_b200 as vt
 
     ws, rank, local = _dist()
+    # VT_BENCH_ONE_GPU=1: every rank on cuda:0 with a gloo process group -- exercises the
+    # N>1 flow (barriers, max-over-ranks, rank-0 reporting) on a 1-GPU box; not a bench number
+    one_gpu = os.environ.get("VT_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     spec = vt.CodeSpec(K_CODE, GENS)
     n = N_STAGES
     bits_true, q = make_stream(torch, n, seed=1234 + rank, device=dev)
@@ -193,7 +201,8 @@ def run_ours(args) -> None:
     if ws > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    red_dev = "cpu" if one_gpu else dev  # (gloo reduces host tensors)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -217,7 +226,7 @@ def run_ours(args) -> None:
     for _ in range(e2e_steps):
         vt.decode_stream_host(q_host, spec, F, V, bits_host=bits_host, nchunks=args.e2e_chunks, stream=stream)
     t_e2e = (time.perf_counter() - t0) / e2e_steps
-    te = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+    te = torch.tensor([t_e2e], dtype=torch.float64, device=red_dev)
     if ws > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = ws * n / float(te.item()) / 1e9

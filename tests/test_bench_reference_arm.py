@@ -1,10 +1,13 @@
-"""bench.py's reference arm under torchrun (CPU only): rank 0 alone times the
-reference decoder's CPU path and prints one JSON line; the other ranks exit 0."""
+"""bench.py under torchrun.  Reference arm (CPU only): rank 0 alone times the
+reference decoder's CPU path and prints one JSON line; the other ranks exit 0.
+Our arm (GPU): the world-size-2 flow on one GPU."""
 import json
 import os
 import socket
 import subprocess
 import sys
+
+import pytest
 
 from conftest import ROOT
 
@@ -27,3 +30,21 @@ def test_reference_arm_world_size_2_prints_one_line():
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
     assert d["ber"]["bits"] > 0
+
+
+@pytest.mark.gpu
+def test_ours_arm_world_size_2_flow_on_one_gpu():
+    """The N>1 flow of our arm (barriers, max over ranks, rank-0 line) with both ranks on
+    cuda:0 over gloo (VT_BENCH_ONE_GPU=1): the driver's 2/4/8-GPU runs use NCCL, one GPU each."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--no-cpu-baseline", "--no-other-configs"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env=dict(os.environ, VT_BENCH_ONE_GPU="1"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] == 3
+    assert d["e2e"]["bits_match_device_path"] and d["ber"]["ber"] < 1e-2
