@@ -419,7 +419,8 @@ class Gen16:
         SQ = S // 16  # uint4 of history words per group per thread
         e = self.emit
         e(f'extern "C" __global__ void __launch_bounds__({NT}, {MINB16}) {name}(const vt::StreamArgs a) {{')
-        e(f"  constexpr int B = {B}, K = {K}, CH = {CH}, NL = {NL}, NWC = {NWC};")
+        nwc = "" if self.pbr else f", NWC = {NWC}"  # (NWC: chunk-wide realignment only)
+        e(f"  constexpr int B = {B}, K = {K}, CH = {CH}, NL = {NL}{nwc};")
         e("  const int tid = threadIdx.x;")
         e(f"  // dynamic shared memory: LLR staging, 2 buffers (chunk parity) x 2 windows x NL uint4 per")
         e(f"  // thread (column layout), then the traceback ring: TBD x SQ uint4 per thread")
@@ -438,11 +439,13 @@ class Gen16:
         e("  tbA.running = tbB.running = false;")
         e("  tbA.j = tbB.j = 0u; tbA.acc = tbB.acc = 0ull; tbA.lo = tbB.lo = 0; tbA.b = tbB.b = -1;")
         e("  tbA.active = tbB.active = false;")
-        e("  int parity_prev = 0, parity = 0;")
-        e("  uint2 nxtA = make_uint2(0u, 0u), aftA = nxtA, nxtB = nxtA, aftB = nxtA;")
-        e("  int tbb = -1;  // next group of the previous tile to trace (both windows step in lockstep)")
-        e("  int tbr = 0;   // traceback ring entry holding group tbb")
-        e("  const char* const slotc = reinterpret_cast<const char*>(slot);")
+        e("  int parity = 0;")
+        if self.GPB % 2:
+            e("  uint2 nxtA = make_uint2(0u, 0u), aftA = nxtA, nxtB = nxtA, aftB = nxtA;")
+        else:
+            e("  int tbb = -1;  // next group of the previous tile to trace (both windows step in lockstep)")
+            e("  int tbr = 0;   // traceback ring entry holding group tbb")
+            e("  const char* const slotc = reinterpret_cast<const char*>(slot);")
         if self.tc:
             TCN = self.TCN
             e(f"  // ---- tensor-core branch metrics: per chunk, D[window][4*stage + pattern] = A . Bm with")
@@ -503,31 +506,25 @@ class Gen16:
         e("  // cand(grp, base): the 8-byte word pair holding states base..base+7 (base % 8 == 0)")
         e("  // traced tile: group grp sits at slot position x = txa + txs * grp (tiles alternate the order)")
         e("  int txa = -a.b_lo, txs = 1;  // (initial values keep the idle prefetches inside the slot)")
-        e("  auto cand = [&](int grp, uint32_t base) -> uint2 {")
-        e(f"    const uint32_t off = (uint32_t)(txa + txs * grp) * {SQ * NT * 16}u + (base >> 4) * {NT * 16}u + (base & 8u);")
-        e("    return __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(slot) + off));")
-        e("  };")
-        e(f"  auto tb_advance = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft, int side) {{")
-        e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
-        e("    const uint32_t li = tb.j & 7u;")
-        e("    const uint32_t w = (li & 4u) ? nxt.y : nxt.x;")
-        e(f"    tb.step((w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
-        e("    tb.settle(a);")
-        e("    nxt = aft;")
-        e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
-        e("  };")
-        e(f"  auto tb_step2 = [&](vt::TracebackLite<K, {L}>& tb, uint2& buf, int side) {{")
-        e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
-        e("    const uint32_t li = tb.j & 7u;")
-        e("    const uint32_t w = (li & 4u) ? buf.y : buf.x;")
-        e(f"    tb.step((w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
-        e(f"    if (tb.b - 1 >= a.b_lo) buf = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
-        e("  };")
-        e(f"  auto tb_begin = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft) {{")
-        e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
-        e("    nxt = cand(tb.b, tb.j & ~7u);")
-        e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
-        e("  };")
+        if self.GPB % 2:  # per-window word-pair traceback (odd groups per body)
+            e("  auto cand = [&](int grp, uint32_t base) -> uint2 {")
+            e(f"    const uint32_t off = (uint32_t)(txa + txs * grp) * {SQ * NT * 16}u + (base >> 4) * {NT * 16}u + (base & 8u);")
+            e("    return __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(slot) + off));")
+            e("  };")
+            e(f"  auto tb_advance = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft, int side) {{")
+            e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
+            e("    const uint32_t li = tb.j & 7u;")
+            e("    const uint32_t w = (li & 4u) ? nxt.y : nxt.x;")
+            e(f"    tb.step((w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
+            e("    tb.settle(a);")
+            e("    nxt = aft;")
+            e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
+            e("  };")
+            e(f"  auto tb_begin = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft) {{")
+            e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
+            e("    nxt = cand(tb.b, tb.j & ~7u);")
+            e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
+            e("  };")
         e(f"  const int ng = a.nc * {CH // L};  // history groups per window")
         e(f"  for (int64_t tile = blockIdx.x; tile * {2 * NT} < nwin; tile += gridDim.x, parity ^= 1) {{")
         e(f"    const int64_t wa = tile * {2 * NT} + 2 * tid, wb = wa + 1;")
@@ -538,10 +535,11 @@ class Gen16:
         e("    // the window's whole staged span (16-byte words) lies inside the buffer: unchecked copies")
         e(f"    const int64_t span = (int64_t)a.nc * CH * B + 16 * NL;")
         e("    const bool fastA = oA >= 0 && oA + span <= buf_bytes, fastB = oB >= 0 && oB + span <= buf_bytes;")
-        e("    // 32-bit per-chunk bookkeeping: misalignment base and front-padding stages of each window")
-        e("    const int moA = (int)(oA & 15), moB = (int)(oB & 15);")
-        e(f"    const int padA = (int)min(max(gA.s - gA.g0, (int64_t)0), (int64_t){1 << 20}), "
-          f"padB = (int)min(max(gB.s - gB.g0, (int64_t)0), (int64_t){1 << 20});")
+        if self.pbr:
+            e("    // 32-bit per-chunk bookkeeping: misalignment base and front-padding stages of each window")
+            e("    const int moA = (int)(oA & 15), moB = (int)(oB & 15);")
+            e(f"    const int padA = (int)min(max(gA.s - gA.g0, (int64_t)0), (int64_t){1 << 20}), "
+              f"padB = (int)min(max(gB.s - gB.g0, (int64_t)0), (int64_t){1 << 20});")
         m0 = (self.Sb << L) * 0x10001 if self.cheap else 0  # cheap stages need m_i1 + T >= 0 from the start
         e("    " + " ".join(f"uint32_t m{j} = {m0:#x}u;" for j in range(S)))
         e("    uint32_t negR = 0, negE = 0;")
@@ -560,7 +558,8 @@ class Gen16:
             e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
               f"(int64_t){self.CHB});")
         e("    int it_start = it0;")
-        e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
+        if not self.pbr or self.tc:
+            e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
         e("    // chunks are staged two ahead (cp.async groups): chunk k lives in buffer k & 1")
         if self.pbr:
             e(f"    vt::stage_row<NL>(llrA(0), a.llr, buf_bytes, oA, fastA);")
@@ -597,7 +596,8 @@ class Gen16:
         e(f"    int gidx = it0 * {self.GPB};")
         e("    // traceback of the previous tile: one group step per forward group, loads one group ahead")
         e("    for (int c = 0; c < a.nc; ++c) {")
-        e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
+        if self.tc:
+            e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
         if not self.pbr:
             e("      if (c + 2 < a.nc) {")
             e(f"        vt::stage_row_rel<NL>(llrA(c & 1), a.llr, buf_bytes, oA, CH * B * (c + 2), fastA);")
@@ -713,7 +713,6 @@ class Gen16:
             e("    txs = parity ? -1 : 1;")
             e("    tb_begin(tbA, nxtA, aftA);")
             e("    tb_begin(tbB, nxtB, aftB);")
-        e("    parity_prev = parity;")
         e("  }")
         e("  // traceback of the CTA's last tile")
         if self.GPB % 2 == 0:
