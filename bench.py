@@ -302,6 +302,8 @@ def other_configs(torch, vt, dev, steps: int) -> list:
              ("K=9 r1/2 (753,561) V=54", 9, (0o753, 0o561), 1 << 26, 256, 54)]
     for f in (64, 128, 256, 512, 1024):
         cases.append((f"K=7 r1/2 sweep F={f}", 7, GENS, 1 << 26, f, 42))
+    for lw in (16, 18, 22):  # batch sweep at F=256 (2^20 windows is the headline)
+        cases.append((f"K=7 r1/2 sweep windows=2^{lw} (F=256)", 7, GENS, 256 << lw, 256, 42))
     # the same headline code through the other kernel forms (VT_KERNEL_VARIANT)
     cases.append(("K=7 r1/2 F=256 tensor-core branch metrics (16x2tc)", 7, GENS, 1 << 26, 256, 42, "16x2tc"))
     cases.append(("K=7 r1/2 F=256 one window per thread (s32)", 7, GENS, 1 << 26, 256, 42, "s32"))
