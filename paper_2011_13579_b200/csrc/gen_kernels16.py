@@ -103,7 +103,7 @@ class Gen16:
                    for j in range(self.S))
         sbc = delta + 2 * self.dmax
         # (not with xmin: for B = 3 the offset stage needs 64 + 64 combo adds per group,
-        # measured slower than the plain stage: 98.5 vs 100.5 Gbps for K=7 r1/3)
+        # measured slower than the plain stage: 120.0 vs 123.6 Gbps for K=7 r1/3)
         self.cheap = (not self.xmin and self.L == 3 and self.GPB % 2 == 0 and comp and
                       sbc + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)))
         if self.xmin:  # the minimum renormalises to 0
@@ -119,7 +119,11 @@ class Gen16:
             self.NL = -(-(15 + self.CH * self.B + 4) // 16)
         self.lines: list[str] = []
         ring = self.TBD * (self.S // 16) if self.GPB % 2 == 0 else 0
-        self.SMEM = (4 * self.NL + ring) * NT * 16  # dynamic shared memory bytes
+        # row stride (uint4) of the per-thread LLR rows: odd, so the realignment's 4-byte loads
+        # (the same byte offset in every thread's row) spread over 8 bank groups (4-way) instead
+        # of 4 (NL = 6: 8-way) or 1 (NL = 8: 32-way)
+        self.RS = self.NL | 1 if self.pbr else self.NL
+        self.SMEM = (4 * self.RS + ring) * NT * 16  # dynamic shared memory bytes
         # tensor-core branch metrics (paper formulation): int8 LLR tile x +-8 codeword matrix
         self.tc = tc
         if tc:
@@ -426,15 +430,15 @@ class Gen16:
         e(f"  // thread (column layout), then the traceback ring: TBD x SQ uint4 per thread")
         e("  extern __shared__ __align__(16) uint4 smem_dyn[];")
         e("  uint4* const s_llr = smem_dyn;")
-        e(f"  uint4* const s_tb = smem_dyn + 4 * NL * {NT};  // (even GPB only)")
+        e(f"  uint4* const s_tb = smem_dyn + {4 * self.RS * NT};  // (even GPB only)")
         e("  (void)s_tb;")
         e("  const uint64_t pol_last = vt::policy_evict_last();")
         e("  const int64_t nwin = a.w1 - a.w0;")
         e("  const int64_t buf_bytes = (a.st1 - a.st0) * B;")
         e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {SQ} * {NT} + tid;")
         e("  // per-thread rows of NL*16 bytes: [buffer][window][thread]")
-        e(f"  auto llrA = [&](int buf) {{ return reinterpret_cast<char*>(s_llr) + ((2 * buf) * {NT} + tid) * (16 * NL); }};")
-        e(f"  auto llrB = [&](int buf) {{ return reinterpret_cast<char*>(s_llr) + ((2 * buf + 1) * {NT} + tid) * (16 * NL); }};")
+        e(f"  auto llrA = [&](int buf) {{ return reinterpret_cast<char*>(s_llr) + ((2 * buf) * {NT} + tid) * {16 * self.RS}; }};")
+        e(f"  auto llrB = [&](int buf) {{ return reinterpret_cast<char*>(s_llr) + ((2 * buf + 1) * {NT} + tid) * {16 * self.RS}; }};")
         e(f"  vt::TracebackLite<K, {L}> tbA, tbB;")
         e("  tbA.running = tbB.running = false;")
         e("  tbA.j = tbB.j = 0u; tbA.acc = tbB.acc = 0ull; tbA.lo = tbB.lo = 0; tbA.b = tbB.b = -1;")

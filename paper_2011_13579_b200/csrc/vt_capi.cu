@@ -89,9 +89,9 @@ int variant_rank(const KernelEntry* e, const char* env) {
   if (env && strcmp(env, "16x2") == 0) return (is16 && !istc) ? 0 : (istc ? 2 : 1);
   if (env && strcmp(env, "s32") == 0) return is16 ? 2 : 0;
   if (istc) return 3;                       // opt-in only
-  // 16x2 preferred for rate 1/2 with 3-bit groups (K=7 r1/2: 162 vs 118 Gbps); K=7 r1/3
-  // in 16x2 (exact-minimum renormalisation) measured 100.5 vs 112.6 Gbps for s32
-  if (is16) return (e->BL >= 3 && e->B == 2) ? 0 : 2;
+  // 16x2 preferred wherever 3-bit history groups fit (K=7 r1/2: 163 vs 118 Gbps; K=7 r1/3
+  // with exact-minimum renormalisation: 124 vs 113 Gbps)
+  if (is16) return e->BL >= 3 ? 0 : 2;
   return 1;
 }
 
