@@ -343,16 +343,24 @@ class Gen16:
             e(f"{ind}offB += pendB;")
         e(f"{ind}{{")
         if self.xmin:  # exact per-half minimum over all states (history bits masked after)
+            # ternary tree min(min(a, b), c): ptxas fuses each into one VIMNMX3.U16x2
             vals = [f"m{j}" for j in range(S)]
             lvl = 0
             while len(vals) > 1:
                 nxt = []
-                for i in range(0, len(vals) - 1, 2):
-                    nm = f"mn{lvl}_{i // 2}"
-                    e(f"{ind}  const uint32_t {nm} = vt::vmin2({vals[i]}, {vals[i + 1]});")
-                    nxt.append(nm)
-                if len(vals) % 2:
-                    nxt.append(vals[-1])
+                i = 0
+                while i < len(vals):
+                    grp = vals[i:i + 3]
+                    if len(grp) == 1:
+                        nxt.append(grp[0])
+                    else:
+                        nm = f"mn{lvl}_{i // 3}"
+                        expr = f"vt::vmin2({grp[0]}, {grp[1]})"
+                        if len(grp) == 3:
+                            expr = f"vt::vmin2({expr}, {grp[2]})"
+                        e(f"{ind}  const uint32_t {nm} = {expr};")
+                        nxt.append(nm)
+                    i += 3
                 vals, lvl = nxt, lvl + 1
             e(f"{ind}  const uint32_t r0 = {vals[0]} & {lm:#x}u;")
         else:

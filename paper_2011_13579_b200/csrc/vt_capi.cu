@@ -90,7 +90,7 @@ int variant_rank(const KernelEntry* e, const char* env) {
   if (env && strcmp(env, "s32") == 0) return is16 ? 2 : 0;
   if (istc) return 3;                       // opt-in only
   // 16x2 preferred wherever 3-bit history groups fit (K=7 r1/2: 163 vs 118 Gbps; K=7 r1/3
-  // with exact-minimum renormalisation: 124 vs 113 Gbps)
+  // with exact-minimum renormalisation: 127.5 vs 113 Gbps)
   if (is16) return e->BL >= 3 ? 0 : 2;
   return 1;
 }
