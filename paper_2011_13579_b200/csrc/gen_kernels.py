@@ -383,6 +383,23 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
         gl = ", ".join(f"{x}u" for x in gens)
         decl.append(f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);')
         reg.append(f"VT_KERNEL(vtk_{name}, nullptr, 0, 0, {NT}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, {g.SQ}, {{{gl}}})")
+        if K in (8, 9):  # packed 16x2 variant over T lanes per window pair
+            import sys
+            here = os.path.dirname(os.path.abspath(__file__))
+            if here not in sys.path:
+                sys.path.insert(0, here)
+            from gen_kernels16m import Gen16M
+            gm = Gen16M(name, K, gens, T)
+            srcm = gm.kernel()
+            pathm = os.path.join(outdir, f"vtk16m_{name}.cu")
+            if not os.path.exists(pathm) or open(pathm).read() != srcm:
+                with open(pathm, "w") as fh:
+                    fh.write(srcm)
+            files.append(pathm)
+            decl.append(f'extern "C" __global__ void vtk16m_{name}(const vt::StreamArgs a);')
+            decl.append(f'extern "C" __global__ void vtk16mnf_{name}(const vt::StreamArgs a);')
+            reg.append(f"VT_KERNEL(vtk16m_{name}, &vtk16mnf_{name}, {gm.SMEM}, 0, 128, {K}, {len(gens)}, {T}, 2, "
+                       f"{gm.SL}, {gm.CH}, {gm.L}, {gm.SQ}, {{{gl}}})")
         if K == 7:  # packed 16x2 variant: two windows per thread
             import sys
             here = os.path.dirname(os.path.abspath(__file__))

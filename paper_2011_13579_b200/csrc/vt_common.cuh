@@ -195,6 +195,23 @@ __device__ __forceinline__ void stage_row(char* row, const int8_t* __restrict__ 
   }
 }
 
+// stage_row split over the T lanes of a window group: lane t copies chunks t, t+T, ...
+// (the row is then read by all T lanes: wait for the copies, then __syncwarp)
+template <int NL, int T>
+__device__ __forceinline__ void stage_row_part(char* row, const int8_t* __restrict__ llr, int64_t buf_bytes,
+                                               int64_t o, bool fast, int t) {
+  const int64_t base = (o >> 4) << 4;
+#pragma unroll
+  for (int i0 = 0; i0 < NL; i0 += T) {
+    const int i = i0 + t;
+    if (i < NL) {
+      const int64_t a = base + 16 * i;
+      const bool ok = fast || ((a >= 0) && (a < buf_bytes));
+      cp_async16(row + 16 * i, llr + (ok ? a : 0), ok ? 16 : 0, 0);
+    }
+  }
+}
+
 // stage_row at byte offset o = o0 + rel (rel 32-bit): the fast path needs no 64-bit
 // offset arithmetic beyond one pointer add
 template <int NL>
