@@ -304,9 +304,11 @@ class Gen16M(Gen16):
         e(f"{ind}}}")
         e(f"{ind}++gidx;")
 
-    def exchange(self, ind: str, lo: int) -> None:
-        """Shared-memory transpose of the pair's metrics from partition `lo` to the top
-        partition (the s32 kernels' conflict-free layout, gen_kernels.Gen.exchange)."""
+    def exchange_write(self, ind: str, lo: int) -> None:
+        """Transpose, write half: the pair's metrics in partition `lo` go to the transpose
+        buffer at their top-partition positions (the s32 kernels' conflict-free layout,
+        gen_kernels.Gen.exchange).  The next body starts with exchange_read, so no metric
+        register is carried around the body loop (no register moves after LDS.128)."""
         top, G, SL = self.top, self.G, self.SL
         e = self.emit
         e(f"{ind}// transpose: partition [{lo},{lo + self.tau}) -> [{top},{top + self.tau})")
@@ -326,10 +328,15 @@ class Gen16M(Gen16):
             else:
                 e(f"{ind}xw[{off} + (t << {lo})] = m{r};")
                 r += 1
+
+    def exchange_read(self, ind: str, decl: bool = True) -> None:
+        """Transpose, read half: this lane's 64 top-partition slots (LDS.128)."""
+        e = self.emit
         e(f"{ind}__syncwarp(pm);")
-        for r in range(0, SL, 4):
-            e(f"{ind}{{ const uint4 v = *reinterpret_cast<const uint4*>(xr + {r}); "
-              f"m{r} = v.x; m{r + 1} = v.y; m{r + 2} = v.z; m{r + 3} = v.w; }}")
+        for r in range(0, self.SL, 4):
+            e(f"{ind}const uint4 v{r} = *reinterpret_cast<const uint4*>(xr + {r});")
+        ty = "uint32_t " if decl else ""
+        e(f"{ind}" + " ".join(f"{ty}m{r + i} = v{r}.{'xyzw'[i]};" for r in range(0, self.SL, 4) for i in range(4)))
 
     def kernel(self) -> str:
         self.lines = []
@@ -400,7 +407,8 @@ class Gen16M(Gen16):
         e(f"    const int padA = (int)min(max(gA.s - gA.g0, (int64_t)0), (int64_t){1 << 20}), "
           f"padB = (int)min(max(gB.s - gB.g0, (int64_t)0), (int64_t){1 << 20});")
         m0 = (self.Sb << L) * 0x10001
-        e("    " + " ".join(f"uint32_t m{r} = {m0:#x}u;" for r in range(SL)))
+        e("    __syncwarp(pm);  // the previous tile's final metrics are read")
+        e(f"    for (int r = 0; r < {SL}; r += 4) *reinterpret_cast<uint4*>(xw + t * {self.G} + r) = make_uint4({m0:#x}u, {m0:#x}u, {m0:#x}u, {m0:#x}u);")
         e("    uint32_t negR = 0, negE = 0;")
         if self.fm:
             e(f"    int64_t offA = {-self.Sb}, offB = {-self.Sb}, pendA = 0, pendB = 0;")
@@ -425,6 +433,7 @@ class Gen16M(Gen16):
         for w in ("A", "B"):
             e(f"        vt::realign_row_at<{self.NWB}>(cur{w}, llr{w}(c & 1), ((mo{w} + CH * B * c) & 15) + {P * B} * it, "
               f"min(max((pad{w} - CH * c - {P} * it) * B, 0), {P * B}));")
+        self.exchange_read("        ")
         names = [f"m{r}" for r in range(SL)]
         deferred: list = []
         for q in range(P):
@@ -436,7 +445,7 @@ class Gen16M(Gen16):
                     e(f"        m{r} = {names[r]};")
                 names = [f"m{r}" for r in range(SL)]
                 self.group_end("        ", q // L)
-        self.exchange("        ", self.top - P)
+        self.exchange_write("        ", self.top - P)
         e("      }")
         e("      it_start = 0;")
         e("      tb.settle(a);")
@@ -459,6 +468,7 @@ class Gen16M(Gen16):
         e("    tb.b = tbb;")
         e("    if (tb.running) tb.drain_unstored(a);")
         e("    // final states: argmax per window over all lanes, lowest index on ties (reference.py:138)")
+        self.exchange_read("    ")
         e("    uint32_t bestA = 0, bestB = 0;")
         for r in range(SL):
             st = self.state_of(r, 0, self.top)
