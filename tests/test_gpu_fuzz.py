@@ -67,3 +67,48 @@ def test_fuzz_window_ranges(case, variant, monkeypatch, tmp_path):
     words = fileio.decode_llr_file(str(p), "single", CodeSpec(K, GENS), f, v, windows_per_piece=per)
     got = np.unpackbits(words.view(np.uint8), count=n, bitorder="little")
     np.testing.assert_array_equal(got, oracle.decode_stream(q, K, GENS, f, v, threads=8))
+
+
+# K=8 / K=9: the multi-lane 16x2 kernels (states over 2 / 4 lanes, shared-memory transpose,
+# exact-minimum renormalisation) and the s32 kernels
+_CODES89 = {"k9r2": (9, (0o753, 0o561)), "k8r2": (8, (0o247, 0o371))}
+
+
+def _llr_code(n, kind, seed, k, gens):
+    rng = np.random.default_rng(seed)
+    if kind.startswith("awgn"):
+        _, q = oracle.synthetic_stream(n, k, gens, ebn0_db=float(kind[4:]), seed=seed & 0xFFFF, scale=16.0)
+        return q
+    return _llr(n, kind, seed)
+
+
+@pytest.mark.parametrize("variant", ["16x2", "s32"])
+@pytest.mark.parametrize("code", sorted(_CODES89))
+@pytest.mark.parametrize("case", _cases(seed=99, count=12), ids=lambda c: f"n{c[0]}-F{c[1]}-V{c[2]}-{c[3]}")
+def test_fuzz_stream_k89(case, code, variant, monkeypatch):
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    monkeypatch.setenv("VT_KERNEL_VARIANT", variant)
+    k, gens = _CODES89[code]
+    n, f, v, kind, seed = case
+    q = _llr_code(n, kind, seed, k, gens)
+    want = oracle.decode_stream(q, k, gens, f, v, threads=8)
+    words = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(k, gens), f, v)
+    got = np.unpackbits(words.cpu().numpy().view(np.uint8), count=n, bitorder="little")
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("case", _cases(seed=5, count=4), ids=lambda c: f"n{c[0]}-F{c[1]}-V{c[2]}-{c[3]}")
+def test_fuzz_window_ranges_k9(case, tmp_path):
+    """Window-range launches of the multi-lane kernel on stage sub-buffers."""
+    from paper_2011_13579_b200 import CodeSpec, fileio
+    k, gens = _CODES89["k9r2"]
+    n, f, v, kind, seed = case
+    q = _llr_code(n, kind, seed, k, gens)
+    p = tmp_path / "q.llr"
+    fileio.write_llr_file(q.astype(np.float64).reshape(-1), str(p), "single")
+    per = max(1, (-(-n // f)) // 3)
+    words = fileio.decode_llr_file(str(p), "single", CodeSpec(k, gens), f, v, windows_per_piece=per)
+    got = np.unpackbits(words.view(np.uint8), count=n, bitorder="little")
+    np.testing.assert_array_equal(got, oracle.decode_stream(q, k, gens, f, v, threads=8))

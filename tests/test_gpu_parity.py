@@ -158,11 +158,12 @@ def test_final_metrics_match_oracle(vt):
 
 
 @pytest.mark.parametrize("variant", ["16x2", "s32", "16x2tc"])
-@pytest.mark.parametrize("code", ["k7r2", "k7r3"])
+@pytest.mark.parametrize("code", ["k7r2", "k7r3", "k8r2", "k9r2"])
 @pytest.mark.parametrize("fv", [(256, 42), (100, 20), (37, 5)])
 def test_kernel_variants_match_oracle(vt, code, fv, variant, monkeypatch):
-    """Both K=7 kernel forms are bit-exact: the default two-windows-per-thread 16x2
-    kernels and the one-window-per-thread s32 kernels (VT_KERNEL_VARIANT=s32)."""
+    """Every kernel form is bit-exact (decoded bits and final metrics): the 16x2 kernels
+    (two windows per thread; K=8/9 spread over 2/4 lanes), the one-window-per-thread s32
+    kernels (VT_KERNEL_VARIANT=s32) and the tensor-core branch-metric form (K=7 r1/2)."""
     monkeypatch.setenv("VT_KERNEL_VARIANT", variant)
     k, gens = code_params(CODES, code)
     spec = vt.CodeSpec(k, gens)

@@ -1,8 +1,8 @@
 """The 16x2 kernels keep path metrics in 16-bit halves; their range argument
-(gen_kernels16.py) bounds the K=7 metric spread by 256 * W6, W6 the code's
-maximum output-difference weight over 6 stages.  (171,133) renormalises by
-state 0 (span 2*Delta), the r1/3 (133,171,165) by the exact minimum (span
-Delta).  CPU: the bound's inputs and adversarial streams' spreads; GPU: those
+(gen_kernels16.py, gen_kernels16m.py) bounds the metric spread by 256 * W, W
+the code's maximum output-difference weight over K-1 stages.  (171,133)
+renormalises by state 0 (span 2*Delta); the r1/3 (133,171,165) and K=9
+(753,561) by the exact minimum (span Delta).  CPU: the bound's inputs and adversarial streams' spreads; GPU: those
 streams decode exactly."""
 import os
 
@@ -12,8 +12,8 @@ import pytest
 from conftest import ROOT
 from oracle import oracle
 
-CODES = {"k7r2": ((0o171, 0o133), 11, 1500), "k7r3": ((0o133, 0o171, 0o165), 15, 2500)}
-K = 7
+CODES = {"k7r2": (7, (0o171, 0o133), 11, 1500), "k7r3": (7, (0o133, 0o171, 0o165), 15, 2500),
+         "k9r2": (9, (0o753, 0o561), 13, 2000)}
 
 
 def _adv(name):
@@ -29,7 +29,7 @@ def _gen16():
 
 def test_spread_bound_inputs():
     spread_weight, Gen16 = _gen16()
-    gens, w6, _ = CODES["k7r2"]
+    _, gens, w6, _ = CODES["k7r2"]
     assert spread_weight(7, gens) == w6
     g = Gen16("k7r2", 7, gens)
     assert g.cheap and not g.xmin and g.L == 3 and g.Sb == 256 * w6 + 512
@@ -39,7 +39,7 @@ def test_spread_bound_inputs():
 
 def test_spread_bound_inputs_r13_exact_min():
     spread_weight, Gen16 = _gen16()
-    gens, w6, _ = CODES["k7r3"]
+    _, gens, w6, _ = CODES["k7r3"]
     assert spread_weight(7, gens) == w6
     g = Gen16("k7r3", 7, gens)
     # renormalising by state 0 would need 2*Delta + 3*768 < 2^13 (false); by the exact
@@ -49,18 +49,31 @@ def test_spread_bound_inputs_r13_exact_min():
     assert 256 * w6 + 3 * 768 < (1 << 13)
 
 
+def test_spread_bound_inputs_k9_multilane():
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "paper_2011_13579_b200", "csrc"))
+    from gen_kernels16m import Gen16M
+    spread_weight, _ = _gen16()
+    k, gens, w, _ = CODES["k9r2"]
+    assert spread_weight(k, gens) == w
+    g = Gen16M("k9r2", k, gens, 4)
+    # state-0 renormalisation would need 2*Delta + 3*512 < 2^13: 8192, one short
+    assert 2 * 256 * w + 3 * 512 == (1 << 13)
+    assert g.xmin and g.L == 3 and g.Sb + 256 * w + 3 * 512 < (1 << 13)
+
+
 @pytest.mark.parametrize("name", sorted(CODES))
 def test_adversarial_stream_spread_within_bound(name):
-    gens, w6, floor = CODES[name]
+    k, gens, w6, floor = CODES[name]
     q = np.load(_adv(name))["llr"].astype(np.int64)
     assert q.shape[1] == len(gens)
-    S = 64
+    S = 1 << (k - 1)
 
     def par(x):
         return bin(x).count("1") & 1
-    p0 = np.array([2 * (j % 32) for j in range(S)])
-    sg0 = np.array([[1 - 2 * par(g & ((j >> 5) << 6 | p0[j])) for g in gens] for j in range(S)])
-    sg1 = np.array([[1 - 2 * par(g & ((j >> 5) << 6 | (p0[j] + 1))) for g in gens] for j in range(S)])
+    p0 = np.array([2 * (j % (S // 2)) for j in range(S)])
+    sg0 = np.array([[1 - 2 * par(g & ((j >> (k - 2)) << (k - 1) | p0[j])) for g in gens] for j in range(S)])
+    sg1 = np.array([[1 - 2 * par(g & ((j >> (k - 2)) << (k - 1) | (p0[j] + 1))) for g in gens] for j in range(S)])
     m = np.zeros(S, np.int64)
     worst = 0
     for t in range(q.shape[0]):
@@ -79,10 +92,10 @@ def test_adversarial_stream_decodes_exactly(name, fv, variant, monkeypatch):
     import paper_2011_13579_b200 as vt
     import torch
     monkeypatch.setenv("VT_KERNEL_VARIANT", variant)
-    gens = CODES[name][0]
+    k, gens = CODES[name][:2]
     q = np.load(_adv(name))["llr"]
     f, v = fv
-    want = oracle.decode_stream(q, K, gens, f, v, threads=8)
-    out = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(K, gens), f, v)
+    want = oracle.decode_stream(q, k, gens, f, v, threads=8)
+    out = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(k, gens), f, v)
     got = np.unpackbits(out.cpu().numpy().view(np.uint8), count=q.shape[0], bitorder="little")
     np.testing.assert_array_equal(got, want)
