@@ -37,10 +37,10 @@
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).
  *   - Kernel form (same bits, different speed): the environment variable
  *     VT_KERNEL_VARIANT = 16x2 | s32 | 16x2tc forces two windows per thread in
- *     packed 16-bit halves, one window per thread with 32-bit metrics, or 16x2
- *     with tensor-core (tcgen05 kind::i8) branch metrics; by default 16x2 is
- *     used where it exists with 3-bit history groups (K=7 rate 1/2), s32
- *     otherwise.
+ *     packed 16-bit halves (K=8/9: per group of 2/4 lanes), one window per
+ *     thread with 32-bit metrics, or 16x2 with tensor-core (tcgen05 kind::i8)
+ *     branch metrics (K=7 r1/2); by default 16x2 is used where it exists
+ *     (K=7 rate 1/2 and 1/3, K=8, K=9), s32 otherwise (K<=6).
  */
 #ifndef VITERTILE_B200_H
 #define VITERTILE_B200_H

@@ -76,12 +76,12 @@ const KernelEntry* registry(int* n) {
   return table;
 }
 
-// Kernel variant: "16x2" (two windows per thread in packed 16-bit halves), "s32" (one
-// window per thread, 32-bit metrics) or "16x2tc" (16x2 with the branch metrics of each
-// 12-stage chunk computed on the tensor cores: tcgen05 kind::i8, the paper's LLR x
-// codeword-matrix contraction).  Default: 16x2 where it exists with >= 3-bit history
-// groups (K=7 rate 1/2: measured fastest); s32 otherwise (K=7 rate 1/3 needs 2-bit
-// groups, whose group-end work makes the 16x2 form slower).  VT_KERNEL_VARIANT forces one.
+// Kernel variant: "16x2" (two windows per thread -- per group of 2/4 lanes for K=8/9 --
+// in packed 16-bit halves), "s32" (one window per thread, 32-bit metrics) or "16x2tc"
+// (16x2 with the branch metrics of each 12-stage chunk computed on the tensor cores:
+// tcgen05 kind::i8, the paper's LLR x codeword-matrix contraction).  Default: 16x2
+// where it exists with 3-bit history groups (measured fastest for every such code);
+// s32 otherwise.  VT_KERNEL_VARIANT forces one.
 int variant_rank(const KernelEntry* e, const char* env) {
   // lower is better; entries of the requested variant win, then the default order
   const bool is16 = e->WPT > 1, istc = e->tc != 0;
@@ -90,7 +90,7 @@ int variant_rank(const KernelEntry* e, const char* env) {
   if (env && strcmp(env, "s32") == 0) return is16 ? 2 : 0;
   if (istc) return 3;                       // opt-in only
   // 16x2 preferred wherever 3-bit history groups fit (K=7 r1/2: 163 vs 118 Gbps; K=7 r1/3
-  // with exact-minimum renormalisation: 127.5 vs 113 Gbps)
+  // with exact-minimum renormalisation: 127.5 vs 113; K=9 over 4 lanes: 32.3 vs 25.1)
   if (is16) return e->BL >= 3 ? 0 : 2;
   return 1;
 }
