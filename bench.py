@@ -297,9 +297,10 @@ def run_ours(args) -> None:
 def other_configs(torch, vt, dev, steps: int) -> list:
     """BASELINE.json configs 3-5 on one GPU (reported beside the headline; not the headline metric)."""
     out = []
-    cases = [("K=7 r1/3 (133,171,165)", 7, (0o133, 0o171, 0o165), 1 << 26, 256, 42),
-             ("K=9 r1/2 (753,561)", 9, (0o753, 0o561), 1 << 26, 256, 42),
-             ("K=9 r1/2 (753,561) V=54", 9, (0o753, 0o561), 1 << 26, 256, 54)]
+    # configs 3 and 4 at the headline's batch (2^20 windows of F=256)
+    cases = [("K=7 r1/3 (133,171,165)", 7, (0o133, 0o171, 0o165), 1 << 28, 256, 42),
+             ("K=9 r1/2 (753,561)", 9, (0o753, 0o561), 1 << 28, 256, 42),
+             ("K=9 r1/2 (753,561) V=54", 9, (0o753, 0o561), 1 << 28, 256, 54)]
     for f in (64, 128, 256, 512, 1024):
         cases.append((f"K=7 r1/2 sweep F={f}", 7, GENS, 1 << 26, f, 42))
     for lw in (16, 18, 22):  # batch sweep at F=256 (2^20 windows is the headline)
