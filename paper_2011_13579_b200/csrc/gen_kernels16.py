@@ -87,7 +87,10 @@ class Gen16:
         self.GPB = self.P // self.L  # history groups per body
         # per-body LLR realignment from the staged rows (4-body chunks: half the per-chunk
         # bookkeeping per group, 3 LLR words per window in registers instead of 6)
-        self.pbr = (not tc) and self.GPB % 2 == 0
+        # even groups per body: the traceback ring alternates statically (odd counts, i.e.
+        # 2-bit groups, are left to the s32 kernels: generate() checks `supported`)
+        self.supported = self.GPB % 2 == 0
+        self.pbr = not tc
         self.CHB = int(os.environ.get("VT_CHB16", "6")) if self.pbr else CH_BODIES  # 6: measured best (4: -1%, 8: -13%)
         self.CH = self.P * self.CHB  # LLR chunk (stages)
         self.GPB = self.P // self.L  # history groups per body
@@ -104,7 +107,7 @@ class Gen16:
         sbc = delta + 2 * self.dmax
         # (not with xmin: for B = 3 the offset stage needs 64 + 64 combo adds per group,
         # measured slower than the plain stage: 120.0 vs 123.6 Gbps for K=7 r1/3)
-        self.cheap = (not self.xmin and self.L == 3 and self.GPB % 2 == 0 and comp and
+        self.cheap = (not self.xmin and self.L == 3 and self.supported and comp and
                       sbc + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)))
         if self.xmin:  # the minimum renormalises to 0
             self.Sb = 0
@@ -118,7 +121,7 @@ class Gen16:
         if self.pbr:  # a body's words start anywhere in the row: 15 + CH*B bytes + one word of lookahead
             self.NL = -(-(15 + self.CH * self.B + 4) // 16)
         self.lines: list[str] = []
-        ring = self.TBD * (self.S // 16) if self.GPB % 2 == 0 else 0
+        ring = self.TBD * (self.S // 16)
         # row stride (uint4) of the per-thread LLR rows: odd, so the realignment's 4-byte loads
         # (the same byte offset in every thread's row) spread over 8 bank groups (4-way) instead
         # of 4 (NL = 6: 8-way) or 1 (NL = 8: 32-way)
@@ -374,11 +377,7 @@ class Gen16:
         e(f"{ind}}}")
         e(f"{ind}// one traceback step per window of the previous tile (fields prefetched two groups")
         e(f"{ind}// ahead: the 2^L candidate states of a group are consecutive)")
-        if self.GPB % 2 == 0:  # static buffer alternation: no register copy of an in-flight load
-            self.tb_step_both(ind, ge % 2)
-        else:
-            e(f"{ind}tb_advance(tbA, nxtA, aftA, 0);")
-            e(f"{ind}tb_advance(tbB, nxtB, aftB, 16);")
+        self.tb_step_both(ind, ge % 2)
         e(f"{ind}if (gidx >= a.b_lo) {{")
         e(f"{ind}  const int gs = gidx - a.b_lo;")
         e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {S // 16} * {NT};")
@@ -397,18 +396,6 @@ class Gen16:
             e(f"{ind}  m{j} = vt::mad_u32(h{j}, 0xFFFFFFFFu, m{j});")
         e(f"{ind}}}")
         e(f"{ind}++gidx;")
-
-    def shift_cur(self, ind: str) -> None:
-        nb = self.P * self.B
-        qw, rb = nb // 4, nb % 4
-        for arr in ("curA", "curB"):
-            for i in range(self.NWC):
-                a = f"{arr}[{i + qw}]" if i + qw < self.NWC else "0u"
-                if rb == 0:
-                    self.emit(f"{ind}{arr}[{i}] = {a};")
-                else:
-                    b = f"{arr}[{i + qw + 1}]" if i + qw + 1 < self.NWC else "0u"
-                    self.emit(f"{ind}{arr}[{i}] = __funnelshift_r({a}, {b}, {8 * rb});")
 
     def kernel(self) -> str:
         """Both variants: vtk16_<code> (tracks final metrics when a.final_metric is set)
@@ -452,12 +439,9 @@ class Gen16:
         e("  tbA.j = tbB.j = 0u; tbA.acc = tbB.acc = 0ull; tbA.lo = tbB.lo = 0; tbA.b = tbB.b = -1;")
         e("  tbA.active = tbB.active = false;")
         e("  int parity = 0;")
-        if self.GPB % 2:
-            e("  uint2 nxtA = make_uint2(0u, 0u), aftA = nxtA, nxtB = nxtA, aftB = nxtA;")
-        else:
-            e("  int tbb = -1;  // next group of the previous tile to trace (both windows step in lockstep)")
-            e("  int tbr = 0;   // traceback ring entry holding group tbb")
-            e("  const char* const slotc = reinterpret_cast<const char*>(slot);")
+        e("  int tbb = -1;  // next group of the previous tile to trace (both windows step in lockstep)")
+        e("  int tbr = 0;   // traceback ring entry holding group tbb")
+        e("  const char* const slotc = reinterpret_cast<const char*>(slot);")
         if self.tc:
             TCN = self.TCN
             e(f"  // ---- tensor-core branch metrics: per chunk, D[window][4*stage + pattern] = A . Bm with")
@@ -515,28 +499,8 @@ class Gen16:
             e("    }")
             e("  };")
         e("  // history words of group grp: 4 states per 32-bit word (L bits each, +16 for window B);")
-        e("  // cand(grp, base): the 8-byte word pair holding states base..base+7 (base % 8 == 0)")
         e("  // traced tile: group grp sits at slot position x = txa + txs * grp (tiles alternate the order)")
         e("  int txa = -a.b_lo, txs = 1;  // (initial values keep the idle prefetches inside the slot)")
-        if self.GPB % 2:  # per-window word-pair traceback (odd groups per body)
-            e("  auto cand = [&](int grp, uint32_t base) -> uint2 {")
-            e(f"    const uint32_t off = (uint32_t)(txa + txs * grp) * {SQ * NT * 16}u + (base >> 4) * {NT * 16}u + (base & 8u);")
-            e("    return __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const char*>(slot) + off));")
-            e("  };")
-            e(f"  auto tb_advance = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft, int side) {{")
-            e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
-            e("    const uint32_t li = tb.j & 7u;")
-            e("    const uint32_t w = (li & 4u) ? nxt.y : nxt.x;")
-            e(f"    tb.step((w >> (side + {L} * (li & 3u))) & {(1 << L) - 1}u);")
-            e("    tb.settle(a);")
-            e("    nxt = aft;")
-            e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
-            e("  };")
-            e(f"  auto tb_begin = [&](vt::TracebackLite<K, {L}>& tb, uint2& nxt, uint2& aft) {{")
-            e("    if (!(tb.running && tb.b >= a.b_lo)) return;")
-            e("    nxt = cand(tb.b, tb.j & ~7u);")
-            e(f"    if (tb.b - 1 >= a.b_lo) aft = cand(tb.b - 1, (tb.j << {L}) & {S - 8}u);")
-            e("  };")
         e(f"  const int ng = a.nc * {CH // L};  // history groups per window")
         e(f"  for (int64_t tile = blockIdx.x; tile * {2 * NT} < nwin; tile += gridDim.x, parity ^= 1) {{")
         e(f"    const int64_t wa = tile * {2 * NT} + 2 * tid, wb = wa + 1;")
@@ -570,7 +534,7 @@ class Gen16:
             e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
               f"(int64_t){self.CHB});")
         e("    int it_start = it0;")
-        if not self.pbr or self.tc:
+        if self.tc:
             e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
         e("    // chunks are staged two ahead (cp.async groups): chunk k lives in buffer k & 1")
         if self.pbr:
@@ -602,25 +566,20 @@ class Gen16:
             e("      }")
             e("      tc_issue(0, a.nc > 1 ? 2 : 1);")
             e("    }")
-        elif not self.pbr:
-            e(f"    vt::realign_row<NWC>(curA, llrA(0), (int)(oA0 & 15), {zb0A});")
-            e(f"    vt::realign_row<NWC>(curB, llrB(0), (int)(oB0 & 15), {zb0B});")
         e(f"    int gidx = it0 * {self.GPB};")
         e("    // traceback of the previous tile: one group step per forward group, loads one group ahead")
         e("    for (int c = 0; c < a.nc; ++c) {")
         if self.tc:
             e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
-        if not self.pbr:
+        if self.tc:
             e("      if (c + 2 < a.nc) {")
             e(f"        vt::stage_row_rel<NL>(llrA(c & 1), a.llr, buf_bytes, oA, CH * B * (c + 2), fastA);")
             e(f"        vt::stage_row_rel<NL>(llrB(c & 1), a.llr, buf_bytes, oB, CH * B * (c + 2), fastB);")
             e("      }")
-        if self.GPB % 2 or self.tc:
+        if self.tc:
             # (tc: chunk c+2 is realigned at the end of THIS chunk, which may run no traceback
             # step at all (leading-padding skip), so the staging needs its own commit group)
             e("      vt::cp_async_commit();")
-        elif not self.pbr:
-            e("      // (no commit here: the staging rides on the next traceback step's commit group)")
         if self.tc:
             e("      vt::tc::mbar_wait(tc_bar + (c & 1), (tc_phase >> (c & 1)) & 1u);  // chunk c's branch metrics")
             e("      tc_phase ^= 1u << (c & 1);")
@@ -647,8 +606,6 @@ class Gen16:
                 self.group_end("        ", q // L)
         if self.tc:
             e(f"        tcA += {4 * P}u;")
-        elif not self.pbr:
-            self.shift_cur("        ")
         e("      }")
         e("      it_start = 0;")
         e("      tbA.settle(a);  // whole words of the previous tile's traceback")
@@ -665,7 +622,7 @@ class Gen16:
             e("        tc_write(c & 1, rA, rB);")
             e("        tc_issue(c & 1, 1);")
             e("      }")
-        elif self.pbr:
+        else:
             e("      // chunk c's rows are consumed: stage chunk c+2 into its buffer (rides on the next")
             e("      // traceback step's commit group, >= 4 steps before chunk c+2 starts)")
             e("      if (c + 2 < a.nc) {")
@@ -673,30 +630,15 @@ class Gen16:
             e(f"        vt::stage_row_rel<NL>(llrB(c & 1), a.llr, buf_bytes, oB, CH * B * (c + 2), fastB);")
             e("      }")
             e(f"      if (c + 1 < a.nc) vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 landed")
-        else:
-            e("      if (c + 1 < a.nc) {")
-            if self.GPB % 2:
-                e("        vt::cp_async_wait_group<1>();")
-            else:
-                e(f"        vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 was committed >= 4 steps ago")
-            e(f"        vt::realign_row<NWC>(curA, llrA((c + 1) & 1), (moA + CH * B * (c + 1)) & 15, "
-              "min(max((padA - CH * (c + 1)) * B, 0), CH * B));")
-            e(f"        vt::realign_row<NWC>(curB, llrB((c + 1) & 1), (moB + CH * B * (c + 1)) & 15, "
-              "min(max((padB - CH * (c + 1)) * B, 0), CH * B));")
-            e("      }")
         e("    }")
         e("    // the previous tile's remaining traceback steps, then its unstored tail")
-        if self.GPB % 2 == 0:
-            e("    while (tbb >= a.b_lo) {")
-            self.tb_step_both("      ", 0)
-            self.tb_step_both("      ", 1)
-            e("      tbA.settle(a);")
-            e("      tbB.settle(a);")
-            e("    }")
-            e("    tbA.b = tbB.b = tbb;")
-        else:
-            e("    while (tbA.running && tbA.b >= a.b_lo) tb_advance(tbA, nxtA, aftA, 0);")
-            e("    while (tbB.running && tbB.b >= a.b_lo) tb_advance(tbB, nxtB, aftB, 16);")
+        e("    while (tbb >= a.b_lo) {")
+        self.tb_step_both("      ", 0)
+        self.tb_step_both("      ", 1)
+        e("      tbA.settle(a);")
+        e("      tbB.settle(a);")
+        e("    }")
+        e("    tbA.b = tbB.b = tbb;")
         e("    if (tbA.running) tbA.drain_unstored(a);")
         e("    if (tbB.running) tbB.drain_unstored(a);")
         e("    // final states: argmax per window, lowest index on ties (reference.py:138)")
@@ -713,31 +655,21 @@ class Gen16:
           e("    }")
         e("    tbA.start(gA, jA, actA, ng, a.N);")
         e("    tbB.start(gB, jB, actB, ng, a.N);")
-        if self.GPB % 2 == 0:
-            e("    txa = parity ? a.nbs - 1 + a.b_lo : -a.b_lo;")
-            e("    txs = parity ? -1 : 1;")
-            e("    tbb = ng - 1;")
-            e("    tbr = 0;")
-            for r in range(self.TBD):
-                self.tb_fetch("    ", f"tbb - {r}", f"{r}")
-        else:
-            e("    txa = parity ? a.nbs - 1 + a.b_lo : -a.b_lo;")
-            e("    txs = parity ? -1 : 1;")
-            e("    tb_begin(tbA, nxtA, aftA);")
-            e("    tb_begin(tbB, nxtB, aftB);")
+        e("    txa = parity ? a.nbs - 1 + a.b_lo : -a.b_lo;")
+        e("    txs = parity ? -1 : 1;")
+        e("    tbb = ng - 1;")
+        e("    tbr = 0;")
+        for r in range(self.TBD):
+            self.tb_fetch("    ", f"tbb - {r}", f"{r}")
         e("  }")
         e("  // traceback of the CTA's last tile")
-        if self.GPB % 2 == 0:
-            e("  while (tbb >= a.b_lo) {")
-            self.tb_step_both("    ", 0)
-            self.tb_step_both("    ", 1)
-            e("    tbA.settle(a);")
-            e("    tbB.settle(a);")
-            e("  }")
-            e("  tbA.b = tbB.b = tbb;")
-        else:
-            e("  while (tbA.running && tbA.b >= a.b_lo) tb_advance(tbA, nxtA, aftA, 0);")
-            e("  while (tbB.running && tbB.b >= a.b_lo) tb_advance(tbB, nxtB, aftB, 16);")
+        e("  while (tbb >= a.b_lo) {")
+        self.tb_step_both("    ", 0)
+        self.tb_step_both("    ", 1)
+        e("    tbA.settle(a);")
+        e("    tbB.settle(a);")
+        e("  }")
+        e("  tbA.b = tbB.b = tbb;")
         e("  if (tbA.running) tbA.drain_unstored(a);")
         e("  if (tbB.running) tbB.drain_unstored(a);")
         if self.tc:
