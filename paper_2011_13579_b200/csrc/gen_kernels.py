@@ -362,6 +362,15 @@ class Gen:
         return "\n".join(self.lines)
 
 
+def _gen16_supported(name: str, K: int, gens: tuple[int, ...]) -> bool:
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    if here not in sys.path:
+        sys.path.insert(0, here)
+    from gen_kernels16 import Gen16
+    return Gen16(name, K, gens).supported
+
+
 def generate(outdir: str, codes: dict | None = None) -> list[str]:
     codes = codes or STANDARD_CODES
     os.makedirs(outdir, exist_ok=True)
@@ -400,7 +409,7 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
             decl.append(f'extern "C" __global__ void vtk16mnf_{name}(const vt::StreamArgs a);')
             reg.append(f"VT_KERNEL(vtk16m_{name}, &vtk16mnf_{name}, {gm.SMEM}, 0, 128, {K}, {len(gens)}, {T}, 2, "
                        f"{gm.SL}, {gm.CH}, {gm.L}, {gm.SQ}, {{{gl}}})")
-        if K == 7:  # packed 16x2 variant: two windows per thread
+        if K == 7 and _gen16_supported(name, K, gens):  # packed 16x2 variant: two windows per thread
             import sys
             here = os.path.dirname(os.path.abspath(__file__))
             if here not in sys.path:
