@@ -299,9 +299,10 @@ class Gen16M(Gen16):
         for g in range(SQ):
             ws = ", ".join(words[4 * g: 4 * g + 4])
             e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), pol_last);")
-        for r in range(SL):
-            e(f"{ind}  m{r} = vt::mad_u32(h{r}, 0xFFFFFFFFu, m{r});")
         e(f"{ind}}}")
+        # clear unconditionally (warm-up groups carry no decision bits): no phi moves
+        for r in range(SL):
+            e(f"{ind}m{r} &= {lm:#x}u;")
         e(f"{ind}++gidx;")
 
     def exchange_write(self, ind: str, lo: int) -> None:
