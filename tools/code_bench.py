@@ -8,7 +8,8 @@ import shutil
 import subprocess
 import sys
 
-CODES = {"k7r2": (7, (0o171, 0o133)), "k7r3": (7, (0o133, 0o171, 0o165)), "k9r2": (9, (0o753, 0o561))}
+CODES = {"k7r2": (7, (0o171, 0o133)), "k7r3": (7, (0o133, 0o171, 0o165)), "k9r2": (9, (0o753, 0o561)),
+         "k8r2": (8, (0o247, 0o371)), "k5r2": (5, (0o23, 0o35))}
 
 
 def one(code, log2n, f, v, variant, steps):
