@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -120,10 +121,16 @@ int validate(const vt_code* c) {
   return VT_OK;
 }
 
-int device_sms() {
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;
+// Per (kernel entry, device) launch facts, computed once: the dynamic shared memory
+// opt-in (cudaFuncSetAttribute) and the CTA capacity sms * occupancy.  Small calls
+// (one frame) are host-bound, so these stay off the per-call path.
+constexpr int kMaxEntries = 64, kMaxDevices = 64;
+std::atomic<int> g_cap[kMaxEntries][kMaxDevices];  // 0: not yet computed
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  return dev;
 }
 
 // opt the kernels into their dynamic shared memory (above the 48 KB default); idempotent
@@ -134,19 +141,35 @@ void prepare(const KernelEntry* k) {
   }
 }
 
-int ctas_per_sm(const KernelEntry* k) {
+// CTAs that run concurrently on the device (prepares the kernel on first use per device)
+int64_t cta_capacity(const KernelEntry* k) {
   const char* env = getenv("VT_CTAS_PER_SM");
-  if (env && atoi(env) > 0) return atoi(env);
+  int n = 0;
+  const int idx = (int)(k - registry(&n));
+  const int dev = current_device();
+  const bool cacheable = !(env && atoi(env) > 0) && idx >= 0 && idx < kMaxEntries && dev < kMaxDevices;
+  if (cacheable) {
+    const int c = g_cap[idx][dev].load(std::memory_order_acquire);
+    if (c > 0) return c;
+  }
   prepare(k);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->nt, k->smem) != cudaSuccess || occ < 1) occ = 1;
-  return std::min(occ, 4);
+  if (env && atoi(env) > 0) {
+    occ = atoi(env);
+  } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->nt, k->smem) != cudaSuccess || occ < 1) {
+    occ = 1;
+  }
+  const int cap = sms * std::min(occ, 4);
+  if (cacheable) g_cap[idx][dev].store(cap, std::memory_order_release);
+  return cap;
 }
 
 int64_t grid_for(const KernelEntry* k, int64_t nwin) {
   const int64_t wpc = (int64_t)k->nt * k->WPT / k->T;  // windows per CTA
   const int64_t tiles = (nwin + wpc - 1) / wpc;
-  const int64_t cap = (int64_t)device_sms() * ctas_per_sm(k);
+  const int64_t cap = cta_capacity(k);
   return std::max<int64_t>(1, std::min(tiles, cap));
 }
 
@@ -219,7 +242,7 @@ int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, 
   a.nbs = g.nbs;
   void* args[] = {&a};
   const void* fn = (final_metric == nullptr && k->fn_nofm) ? k->fn_nofm : k->fn;
-  prepare(k);
+  cta_capacity(k);  // (prepared once per device)
   cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(k->nt), args, (size_t)k->smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return VT_OK;

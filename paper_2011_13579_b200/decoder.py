@@ -166,12 +166,20 @@ def _stream_ptr(stream) -> ctypes.c_void_p:
     return ctypes.c_void_p(s.cuda_stream)
 
 
+_codes: dict = {}  # (K, generators) -> checked VtCode (read-only once built)
+
+
 def _code(spec: CodeSpec) -> VtCode:
+    key = (int(spec.constraint_length), tuple(int(g) for g in spec.generators))
+    c = _codes.get(key)
+    if c is not None:
+        return c
     c = VtCode.from_spec(spec)
     if not lib().vt_code_supported(ctypes.byref(c)):
         raise NotImplementedError(
             f"no sm_100a kernel was generated for K={spec.constraint_length} generators "
             f"{spec.octal_generators}; add it to csrc/gen_kernels.py STANDARD_CODES and rebuild")
+    _codes[key] = c
     return c
 
 
