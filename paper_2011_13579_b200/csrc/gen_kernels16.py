@@ -1,13 +1,15 @@
 #!/usr/bin/env python3
-"""Generator for the packed 16x2 ACS kernels (two windows per thread), K <= 7.
+"""Generator for the packed 16x2 ACS kernels (two windows per thread), K = 7
+(K = 8, 9: gen_kernels16m.py, the same forms over 2 / 4 lanes).
 
 Each 32-bit register m_j holds the metric of state j for TWO windows: window
 A in the low 16 bits, window B in the high 16 bits.  Both windows walk the
-same trellis, so one `VIADD.16x2` (candidate i1) + one `VIADDMNMX.U16x2`
-(fused add of candidate i0 + unsigned max) advance state j of both windows:
-half the issue slots per state update of the s32 kernels (gen_kernels.py),
-the instruction pair `tools/pipe_bench.cu` measures at 101 state
-updates/cycle/SM.
+same trellis, so one carry-free `IMAD` (candidate i1, FMA pipe) + one
+`VIADDMNMX.U16x2` (fused add of candidate i0 + unsigned max, ALU pipe) advance
+state j of both windows: half the issue slots per state update of the s32
+kernels (gen_kernels.py).  `tools/pipe_bench.cu` measures the VIADD.16x2 +
+VIADDMNMX.U16x2 pair at 101 state updates/cycle/SM (the roofline peak);
+the cheap middle stage (stage()) needs only the VIADDMNMX.
 
 Per 16-bit half:  U = Lambda * 2^L + h  (unsigned), where
   * h (L bits) records the survivor decisions of the current L-stage history
@@ -23,7 +25,8 @@ Per 16-bit half:  U = Lambda * 2^L + h  (unsigned), where
 At each group end the L-bit fields are masked out, packed 4 states per word
 (12 bits per half), streamed to the scratch slot and cleared.  The traceback
 walks groups: j_prev = ((j << L) | h) & (S-1), decoded bits =
-(j >> (K-1-L)) & (2^L - 1) (vt_common.cuh Traceback<K, L>).
+(j >> (K-1-L)) & (2^L - 1) (vt_common.cuh TracebackLite<K, L>), fed by a
+shared-memory ring of whole history groups prefetched 4 groups ahead.
 """
 from __future__ import annotations
 
