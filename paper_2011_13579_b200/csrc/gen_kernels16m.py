@@ -67,7 +67,7 @@ class Gen16M(Gen16):
         assert self.Sb + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)), "metric range"
         self.pbr = True
         self.tc = False
-        self.CHB = 6
+        self.CHB = int(os.environ.get("VT_CHB16M", "6"))  # 6-body chunks (4: -2%, 10: +0.2%)
         self.CH = self.P * self.CHB
         self.NWB = -(-self.P * self.B // 4)
         self.NL = -(-(15 + self.CH * self.B + 4) // 16)
