@@ -392,13 +392,14 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
         gl = ", ".join(f"{x}u" for x in gens)
         decl.append(f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);')
         reg.append(f"VT_KERNEL(vtk_{name}, nullptr, 0, 0, {NT}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, {g.SQ}, {{{gl}}})")
-        if K in (8, 9):  # packed 16x2 variant over T lanes per window pair
+        lanes = T if K in (8, 9) else 0  # (K=7 over 2 lanes measured 97.6 vs 165 Gbps: DESIGN §9b)
+        if lanes:  # packed 16x2 variant over T lanes per window pair
             import sys
             here = os.path.dirname(os.path.abspath(__file__))
             if here not in sys.path:
                 sys.path.insert(0, here)
             from gen_kernels16m import Gen16M
-            gm = Gen16M(name, K, gens, T)
+            gm = Gen16M(name, K, gens, lanes)
             srcm = gm.kernel()
             pathm = os.path.join(outdir, f"vtk16m_{name}.cu")
             if not os.path.exists(pathm) or open(pathm).read() != srcm:
@@ -407,7 +408,7 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
             files.append(pathm)
             decl.append(f'extern "C" __global__ void vtk16m_{name}(const vt::StreamArgs a);')
             decl.append(f'extern "C" __global__ void vtk16mnf_{name}(const vt::StreamArgs a);')
-            reg.append(f"VT_KERNEL(vtk16m_{name}, &vtk16mnf_{name}, {gm.SMEM}, 0, 128, {K}, {len(gens)}, {T}, 2, "
+            reg.append(f"VT_KERNEL(vtk16m_{name}, &vtk16mnf_{name}, {gm.SMEM}, 0, 128, {K}, {len(gens)}, {lanes}, 2, "
                        f"{gm.SL}, {gm.CH}, {gm.L}, {gm.SQ}, {{{gl}}})")
         if K == 7 and _gen16_supported(name, K, gens):  # packed 16x2 variant: two windows per thread
             import sys
@@ -446,6 +447,9 @@ def generate(outdir: str, codes: dict | None = None) -> list[str]:
         if not os.path.exists(rpath) or open(rpath).read() != text:
             with open(rpath, "w") as fh:
                 fh.write(text)
+    for stale in set(os.listdir(outdir)) - {os.path.basename(f) for f in files}:  # kernels no longer generated
+        if stale.endswith(".cu"):
+            os.remove(os.path.join(outdir, stale))
     return files
 
 

@@ -47,14 +47,13 @@ class Gen16M(Gen16):
         self.tau = T.bit_length() - 1
         assert 1 << self.tau == T and T > 1
         self.SL = self.S // T
-        assert self.SL == 64, "64 states per lane (the K=7 register budget)"
+        assert self.SL in (32, 64), "32 or 64 states per lane"
         self.SQ = self.SL // 16
         self.top = self.k - self.tau
-        self.P = self.top  # stages per body between transposes
+        self.P = 3 * (self.top // 3)  # stages per body between transposes (whole 3-bit groups)
         self.L = 3
         assert self.P % self.L == 0, "body must hold whole 3-bit groups"
         self.GPB = self.P // self.L
-        assert self.GPB % 2 == 0  # static ring parity (tb_fetch per group end)
         self.dmax = 128 * self.B
         delta = 256 * spread_weight(K, gens)
         self.xmin = True
@@ -227,12 +226,14 @@ class Gen16M(Gen16):
         of lane (j >> lo_g) & (T-1), lo_g = the partition at that group's end."""
         L, S, SQ, T, tau = self.L, self.S, self.SQ, self.T, self.tau
         e = self.emit
-        lo_a, lo_b = self.top - self.L, self.top - 2 * self.L  # even / odd groups
+        assert self.GPB in (1, 2)
+        lo_a = self.top - self.L  # partition at the end of a body's first group
+        lo_b = self.top - 2 * self.L if self.GPB == 2 else lo_a  # ... and of its second
         e(f"{ind}{{  // traceback step (previous tile)")
         e(f"{ind}  vt::cp_async_wait_group<{self.TBD - 1}>();")
         e(f"{ind}  __syncwarp(pm);  // the pair's ring entries for group tbb have landed")
         e(f"{ind}  const uint32_t j = tb.j;")
-        e(f"{ind}  const bool odd = tbb & 1;")
+        e(f"{ind}  const bool odd = {'tbb & 1' if self.GPB == 2 else 'false'};")
         e(f"{ind}  const uint32_t tl = odd ? ((j >> {lo_b}) & {T - 1}u) : ((j >> {lo_a}) & {T - 1}u);")
         e(f"{ind}  const uint32_t r = odd ? (((j >> {lo_b + tau}) << {lo_b}) | (j & {(1 << lo_b) - 1}u)) "
           f": (((j >> {lo_a + tau}) << {lo_a}) | (j & {(1 << lo_a) - 1}u));")
