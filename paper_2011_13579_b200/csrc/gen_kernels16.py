@@ -94,7 +94,10 @@ class Gen16:
         # 2-bit groups, are left to the s32 kernels: generate() checks `supported`)
         self.supported = self.GPB % 2 == 0
         self.pbr = not tc
-        self.CHB = int(os.environ.get("VT_CHB16", "6")) if self.pbr else CH_BODIES  # 6: measured best (4: -1%, 8: -13%)
+        # 5-body (30-stage) chunks: the traceback settles once per chunk, and 5 bodies x 6 bits
+        # + < 32 unwritten bits fit its 64-bit accumulator (6 bodies measured +0.6% but need a
+        # mid-chunk settle, -2.5%)
+        self.CHB = int(os.environ.get("VT_CHB16", "5")) if self.pbr else CH_BODIES
         self.CH = self.P * self.CHB  # LLR chunk (stages)
         self.GPB = self.P // self.L  # history groups per body
         self.Sb = 2 * self.k * self.dmax
@@ -613,6 +616,10 @@ class Gen16:
                 self.group_end("        ", q // L)
         if self.tc:
             e(f"        tcA += {4 * P}u;")
+        if self.CHB > 5:
+            # the 64-bit traceback accumulator holds < 32 unwritten bits after a settle plus
+            # 3 bits per step: settle at least every 5 bodies (10 steps), not only per chunk
+            e(f"        if (it == {self.CHB // 2 - 1}) {{ tbA.settle(a); tbB.settle(a); }}")
         e("      }")
         e("      it_start = 0;")
         e("      tbA.settle(a);  // whole words of the previous tile's traceback")

@@ -66,7 +66,7 @@ class Gen16M(Gen16):
         assert self.Sb + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)), "metric range"
         self.pbr = True
         self.tc = False
-        self.CHB = int(os.environ.get("VT_CHB16M", "6"))  # 6-body chunks (4: -2%, 10: +0.2%)
+        self.CHB = int(os.environ.get("VT_CHB16M", "5"))  # 5-body chunks: one traceback settle per chunk (see Gen16)
         self.CH = self.P * self.CHB
         self.NWB = -(-self.P * self.B // 4)
         self.NL = -(-(15 + self.CH * self.B + 4) // 16)
@@ -448,6 +448,10 @@ class Gen16M(Gen16):
                 names = [f"m{r}" for r in range(SL)]
                 self.group_end("        ", q // L)
         self.exchange_write("        ", self.top - P)
+        if self.CHB * self.GPB > 10:
+            # the 64-bit traceback accumulator holds < 32 unwritten bits after a settle plus
+            # 3 bits per step: settle at least every 10 steps, not only per chunk
+            e(f"        if (it == {self.CHB // 2 - 1}) tb.settle(a);")
         e("      }")
         e("      it_start = 0;")
         e("      tb.settle(a);")

@@ -99,3 +99,21 @@ def test_adversarial_stream_decodes_exactly(name, fv, variant, monkeypatch):
     out = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(k, gens), f, v)
     got = np.unpackbits(out.cpu().numpy().view(np.uint8), count=q.shape[0], bitorder="little")
     np.testing.assert_array_equal(got, want)
+
+
+def test_traceback_accumulator_capacity():
+    """TracebackLite keeps < 32 unwritten bits after a settle in a 64-bit accumulator
+    and gains L bits per traceback step; the 16x2 kernels settle once per LLR chunk
+    (CHB bodies x GPB steps), so a chunk may add at most 33 bits unless the generator
+    emits a mid-chunk settle."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "paper_2011_13579_b200", "csrc"))
+    from gen_kernels16 import Gen16
+    from gen_kernels16m import Gen16M
+    gens = [Gen16("k7r2", 7, (0o171, 0o133)), Gen16("k7r3", 7, (0o133, 0o171, 0o165)),
+            Gen16("k7r2", 7, (0o171, 0o133), tc=True), Gen16M("k9r2", 9, (0o753, 0o561), 4),
+            Gen16M("k8r2", 8, (0o247, 0o371), 2)]
+    for g in gens:
+        per_chunk = g.CHB * g.GPB * g.L
+        src = g.kernel()
+        assert per_chunk <= 33 or "settle(a)" in src.split("it_start = 0;")[0], (g.name, per_chunk)
