@@ -316,7 +316,7 @@ def other_configs(torch, vt, dev, steps: int) -> list:
         if variant:
             os.environ["VT_KERNEL_VARIANT"] = variant
         spec = vt.CodeSpec(k, gens)
-        _, q = make_stream(torch, n, seed=77, device=dev, gens=gens, k=k)
+        bits_true, q = make_stream(torch, n, seed=77, device=dev, gens=gens, k=k)
         o = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev)
         for _ in range(3):
             vt.decode_stream_device(q, spec, f, v, out=o, stream=stream)
@@ -330,9 +330,14 @@ def other_configs(torch, vt, dev, steps: int) -> list:
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
         su = algorithmic_state_updates(n, f, v, 1 << (k - 1))
+        # decoded-bit sanity at Eb/N0 = 3 dB (a kernel regression shows up as a BER jump)
+        shifts = torch.arange(32, device=dev, dtype=torch.int32)
+        dec = ((o.view(-1, 1) >> shifts) & 1).view(-1)[:n].to(torch.uint8)
+        ber = float((dec != bits_true).sum().item()) / n
         out.append({"config": label, "frame_len": f, "overlap": v, "stages": n, "windows": -(-n // f),
                     "value": round(n / (ms * 1e-3) / 1e9, 2), "unit": "Gbps", "ms_per_step": round(ms, 4),
-                    "gstate_updates_per_s": round(su / (ms * 1e-3) / 1e9, 1)})
+                    "gstate_updates_per_s": round(su / (ms * 1e-3) / 1e9, 1), "ber_3db": ber})
+        del dec, bits_true
         if variant:
             if old_env is None:
                 os.environ.pop("VT_KERNEL_VARIANT", None)
