@@ -254,6 +254,11 @@ class Gen:
         e("  };")
         e(f"  for (int64_t tile = blockIdx.x; tile * {WPC} < nwin; tile += gridDim.x, parity ^= 1) {{")
         e(f"    const int64_t wrel = tile * {WPC} + wloc;")
+        e("    // the previous tile's history stores (read back by this tile's traceback steps with")
+        e("    // cp.async, by lane 0 of the window's lanes) are ordered before those reads")
+        e("    __threadfence();")
+        if T > 1:
+            e("    __syncwarp(gmask);")
         e("    const bool active = wrel < nwin;")
         e("    const vt::Window g = vt::window_geometry<BL>(a, a.w0 + (active ? wrel : nwin - 1));")
         e("    const int64_t o0 = (g.g0 - a.st0) * B;")

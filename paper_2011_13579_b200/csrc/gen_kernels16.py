@@ -673,6 +673,11 @@ class Gen16:
         e("    txs = parity ? -1 : 1;")
         e("    tbb = ng - 1;")
         e("    tbr = 0;")
+        e("    // this tile's history stores (STG) must be visible before the ring prefill and the next")
+        e("    // tile's traceback read them back with cp.async: without the fence a fetch issued right")
+        e("    // after the last stores could return stale data (measured: nondeterministic words on")
+        e("    // multi-tile launches)")
+        e("    __threadfence();")
         for r in range(self.TBD):
             self.tb_fetch("    ", f"tbb - {r}", f"{r}")
         e("  }")

@@ -496,6 +496,12 @@ class Gen16M(Gen16):
         e("    txs = parity ? -1 : 1;")
         e("    tbb = ng - 1;")
         e("    tbr = 0;")
+        e("    // this tile's history stores (STG) must be visible before the ring prefill and the next")
+        e("    // tile's traceback read them back with cp.async -- same thread and, for the traceback")
+        e("    // lanes, other lanes of the pair: without the fence a fetch issued right after the last")
+        e("    // stores could return stale data (measured: nondeterministic words on multi-tile launches)")
+        e("    __threadfence();")
+        e("    __syncwarp(pm);")
         for r in range(self.TBD):
             self.tb_fetch("    ", f"tbb - {r}", f"{r}")
         e("  }")

@@ -58,3 +58,62 @@ def test_multi_tile_overlapping_windows(form):
     s0 = ((n - sub) // F) * F
     want = oracle.decode_stream(q[s0:], k, gens, F, V, threads=8)
     np.testing.assert_array_equal(got[s0 + F:], want[F:])
+
+
+@pytest.mark.parametrize("form", [FORMS[0], FORMS[2]], ids=["K7", "K9"])
+def test_multi_tile_final_metrics(form):
+    """decode_batch (final-metric kernels) with several tiles per CTA."""
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    k, gens, wpc, _ = form
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    f, fl = 2 * sms * wpc + 50, 100
+    llrs = np.random.default_rng(k).integers(-128, 128, size=(f, len(gens), fl)).astype(np.int8)
+    bits, metric = vt.decode_batch(llrs.astype(np.float64), vt.CodeSpec(k, gens))
+    sel = np.r_[0:64, f - 64:f]
+    wb, wm = oracle.decode_batch(llrs[sel], k, gens)
+    np.testing.assert_array_equal(bits[sel], wb)
+    np.testing.assert_array_equal(metric[sel], wm.astype(np.float64))
+
+
+@pytest.mark.parametrize("form", [FORMS[0], FORMS[2]], ids=["K7", "K9"])
+def test_multi_tile_window_range_pieces(form, tmp_path):
+    """A long stream decoded as window-range pieces on stage sub-buffers (the file
+    streaming / shard path, several tiles per CTA per piece) equals the whole decode."""
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    from paper_2011_13579_b200 import fileio
+    k, gens, wpc, _ = form
+    F, V = 256, 42
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = 3 * (2 * sms * wpc + 100) * F + 5
+    q = np.random.default_rng(k + 100).integers(-128, 128, size=(n, len(gens))).astype(np.int8)
+    whole = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(k, gens), F, V).cpu().numpy()
+    p = tmp_path / "q.llr"
+    fileio.write_llr_file(q.astype(np.float32).reshape(-1), str(p), "single")
+    per = (2 * sms * wpc + 100)
+    pieces = fileio.decode_llr_file(str(p), "single", vt.CodeSpec(k, gens), F, V, windows_per_piece=per)
+    np.testing.assert_array_equal(pieces, whole)
+
+
+@pytest.mark.parametrize("form", FORMS, ids=lambda f: f"K{f[0]}-{oct(f[1][0])}-{f[3] or 'default'}")
+def test_multi_tile_deterministic(form, monkeypatch):
+    """Repeated decodes of one multi-tile stream (uniform int8 LLRs: ties everywhere)
+    return identical words.  (A history fetch issued right after the tile's last
+    stores once returned stale data without the tile-end memory fence.)"""
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    k, gens, wpc, variant = form
+    if variant:
+        monkeypatch.setenv("VT_KERNEL_VARIANT", variant)
+    F, V = 256, 42
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = 3 * (2 * sms * wpc + 50) * F + 13
+    q = torch.from_numpy(np.random.default_rng(99).integers(-128, 128, size=(n, len(gens))).astype(np.int8)).cuda()
+    spec = vt.CodeSpec(k, gens)
+    ref = vt.decode_stream_device(q, spec, F, V)
+    for _ in range(5):
+        assert int((vt.decode_stream_device(q, spec, F, V) != ref).sum().item()) == 0
