@@ -117,3 +117,50 @@ def test_multi_tile_deterministic(form, monkeypatch):
     ref = vt.decode_stream_device(q, spec, F, V)
     for _ in range(5):
         assert int((vt.decode_stream_device(q, spec, F, V) != ref).sum().item()) == 0
+
+
+@pytest.mark.parametrize("fv", [(200, 20), (100, 130), (33, 7)])
+@pytest.mark.parametrize("form", [FORMS[0], FORMS[2], FORMS[4]], ids=["K7", "K9", "K7-s32"])
+def test_multi_tile_unaligned_frames(form, fv, monkeypatch):
+    """Frames that share output words with their neighbours (atomicOr merges), V > F,
+    several tiles per CTA: deterministic and equal to the oracle on window-aligned
+    sub-streams at both ends."""
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    k, gens, wpc, variant = form
+    if variant:
+        monkeypatch.setenv("VT_KERNEL_VARIANT", variant)
+    F, V = fv
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = (2 * sms * wpc + 200) * F + 3
+    q = np.random.default_rng(F + V + k).integers(-128, 128, size=(n, len(gens))).astype(np.int8)
+    spec = vt.CodeSpec(k, gens)
+    dq = torch.from_numpy(q).cuda()
+    words = vt.decode_stream_device(dq, spec, F, V)
+    assert int((vt.decode_stream_device(dq, spec, F, V) != words).sum().item()) == 0
+    got = np.unpackbits(words.cpu().numpy().view(np.uint8), count=n, bitorder="little")
+    m = max(2, -(-V // F) + 1)  # windows whose left halo is cut in a sub-stream starting at k*F
+    sub = (m + 40) * F
+    want = oracle.decode_stream(q[:sub], k, gens, F, V, threads=8)
+    np.testing.assert_array_equal(got[: sub - m * F], want[: sub - m * F])
+    s0 = ((n - sub) // F) * F
+    want = oracle.decode_stream(q[s0:], k, gens, F, V, threads=8)
+    np.testing.assert_array_equal(got[s0 + m * F:], want[m * F:])
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_multi_tile_host_entry(chunks):
+    """vt_decode_stream_host (pinned host buffers, pipelined pieces) with several tiles
+    per CTA per piece equals the device-resident decode."""
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    F, V = 256, 42
+    n = 3 * (2 * sms * 256 + 100) * F + 9
+    q = np.random.default_rng(chunks).integers(-128, 128, size=(n, 2)).astype(np.int8)
+    spec = vt.default_spec()
+    want = vt.decode_stream_device(torch.from_numpy(q).cuda(), spec, F, V).cpu()
+    got = vt.decode_stream_host(torch.from_numpy(q).pin_memory(), spec, F, V, nchunks=chunks)
+    assert torch.equal(got, want)
