@@ -145,14 +145,20 @@ def _torch():
     return torch
 
 
-def _workspace(nbytes: int):
+def _workspace(nbytes: int, stream=None):
+    """Scratch for one launch, one buffer per (device, stream): launches on one stream are
+    ordered, so they may share it; concurrent streams (e.g. worker threads, as
+    framing.decode_stream's workers=) each get their own."""
     torch = _torch()
     dev = torch.cuda.current_device()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    key = (dev, int(s.cuda_stream))
     with _ws_lock:
-        buf = _ws.get(dev)
+        buf = _ws.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=f"cuda:{dev}")
-            _ws[dev] = buf
+            with torch.cuda.stream(s):  # allocated (and later recycled) in the launch stream's order
+                buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=f"cuda:{dev}")
+            _ws[key] = buf
         return buf
 
 
@@ -238,7 +244,7 @@ def decode_stream_device(llr_nb, spec: CodeSpec, frame_len: int, overlap: int, *
         out = torch.zeros(nwords, dtype=torch.int32, device=llr_nb.device)
     nw = -(-n // int(frame_len))
     need = lib().vt_workspace_bytes(ctypes.byref(code), n, int(frame_len), int(overlap), 0, nw)
-    ws = _workspace(need)
+    ws = _workspace(need, stream)
     check(lib().vt_decode_stream(ctypes.byref(code), _ptr(llr_nb), n, int(frame_len), int(overlap), _ptr(out),
                                  _ptr(final_metric), _ptr(ws), ws.numel(), _stream_ptr(stream)))
     return out
@@ -257,7 +263,7 @@ def decode_stream_host(llr_nb_host, spec: CodeSpec, frame_len: int, overlap: int
     if bits_host is None:
         bits_host = torch.empty(nwords, dtype=torch.int32, pin_memory=True)
     dev = torch.cuda.current_device()
-    key = ("host", dev)
+    key = ("host", dev, threading.get_ident())  # the C entry runs on per-thread streams
     with _ws_lock:
         stg = _ws.get(key)
         need_llr = ((n * b + 15) // 16) * 16
@@ -271,7 +277,7 @@ def decode_stream_host(llr_nb_host, spec: CodeSpec, frame_len: int, overlap: int
         w0, w1 = nw * i // nchunks, nw * (i + 1) // nchunks
         if w1 > w0:
             need = max(need, lib().vt_workspace_bytes(ctypes.byref(code), n, int(frame_len), int(overlap), w0, w1))
-    ws = _workspace(need)
+    ws = _workspace(need, stream)
     check(lib().vt_decode_stream_host(ctypes.byref(code), _ptr(llr_nb_host), n, int(frame_len), int(overlap),
                                       _ptr(bits_host), _ptr(stg[0]), _ptr(stg[1]), _ptr(ws), ws.numel(),
                                       int(nchunks), _stream_ptr(stream)))
@@ -431,7 +437,7 @@ def _decode_r4perm_device(llr_nb, spec: CodeSpec, n: int, frame_len: int, overla
     code = _code(spec)
     nw = -(-n // frame_len)
     need = lib().vt_workspace_bytes_r4perm(ctypes.byref(code), n, frame_len, overlap, 0, nw)
-    ws = _workspace(need)
+    ws = _workspace(need, stream)
     prio = np.ascontiguousarray(_r4_priorities(spec))
     check(lib().vt_decode_stream_r4perm(ctypes.byref(code), prio.ctypes.data_as(ctypes.c_void_p), _ptr(llr_nb), 0,
                                         n, n, frame_len, overlap, 0, nw, _ptr(out), _ptr(final_metric), _ptr(ws),

@@ -137,7 +137,7 @@ def decode_llr_file(llr_path: str, dtype: str, spec: CodeSpec, frame_len: int, o
         with torch.cuda.stream(s):
             llr_dev[: q.size].copy_(host[: q.size], non_blocking=True)
         need = lib().vt_workspace_bytes(ctypes.byref(code), n, int(frame_len), int(overlap), w0, w1)
-        ws = _workspace(need)
+        ws = _workspace(need, s)
         check(lib().vt_decode_stream_range(ctypes.byref(code), _ptr(llr_dev), st0, st1, n, int(frame_len),
                                            int(overlap), w0, w1, _ptr(bits), None, _ptr(ws), ws.numel(),
                                            _stream_ptr(s)))

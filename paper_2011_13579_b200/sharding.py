@@ -67,7 +67,7 @@ def decode_stream_sharded(llr_shard_nb, spec, n: int, frame_len: int, overlap: i
     if shard.num_windows == 0:
         return out
     need = lib().vt_workspace_bytes(ctypes.byref(code), n, frame_len, overlap, shard.w0, shard.w1)
-    ws = _workspace(need)
+    ws = _workspace(need, stream)
     check(lib().vt_decode_stream_range(ctypes.byref(code), _ptr(llr_shard_nb), shard.st0, shard.st1, n, frame_len,
                                        overlap, shard.w0, shard.w1, _ptr(out), None, _ptr(ws), ws.numel(),
                                        _stream_ptr(stream)))

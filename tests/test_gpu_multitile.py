@@ -164,3 +164,46 @@ def test_multi_tile_host_entry(chunks):
     want = vt.decode_stream_device(torch.from_numpy(q).cuda(), spec, F, V).cpu()
     got = vt.decode_stream_host(torch.from_numpy(q).pin_memory(), spec, F, V, nchunks=chunks)
     assert torch.equal(got, want)
+
+
+def test_concurrent_threads_and_streams():
+    """Decodes from several host threads, each on its own CUDA stream (device entry)
+    or through the pipelined host entry, overlap on the GPU: each thread has its own
+    scratch (per-stream workspace, per-thread staging) and gets the serial result."""
+    import threading
+
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    spec = vt.default_spec()
+    F, V = 256, 42
+    rng = np.random.default_rng(1)
+    streams_q = [rng.integers(-128, 128, size=(600_000 + 1000 * i, 2)).astype(np.int8) for i in range(4)]
+    want = [vt.decode_stream_device(torch.from_numpy(q).cuda(), spec, F, V).cpu() for q in streams_q]
+    got = [None] * 8
+    errors = []
+
+    def work(i):
+        try:
+            q = streams_q[i % 4]
+            if i < 4:
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    dq = torch.from_numpy(q).cuda(non_blocking=False)
+                    out = vt.decode_stream_device(dq, spec, F, V, stream=s)
+                s.synchronize()
+                got[i] = out.cpu()
+            else:
+                got[i] = vt.decode_stream_host(torch.from_numpy(q).pin_memory(), spec, F, V, nchunks=3).clone()
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    for _ in range(3):
+        threads = [threading.Thread(target=work, args=(i,)) for i in range(8)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        assert not errors, errors
+        for i in range(8):
+            assert torch.equal(got[i], want[i % 4]), i
