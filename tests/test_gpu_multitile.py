@@ -207,3 +207,23 @@ def test_concurrent_threads_and_streams():
         assert not errors, errors
         for i in range(8):
             assert torch.equal(got[i], want[i % 4]), i
+
+
+def test_matrix_r4_optimized_large_batch():
+    """decode_matrix_batch (radix-4 optimised tie order, thread-per-window kernel with
+    several windows per thread) on a batch larger than the grid: every frame equals its
+    own single-frame decode (per-thread scratch reused window after window)."""
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    spec = vt.default_spec()
+    cfg = vt.DecoderConfig(radix=4, optimized=True)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    f, n = 2 * sms * 4 * 128 + 37, 61  # > 1 window per thread; odd length: final radix-2 step
+    rng = np.random.default_rng(4)
+    llrs = rng.integers(-8, 9, size=(f, 2, n)).astype(np.float64)  # tie-heavy
+    res = vt.decode_matrix_batch(llrs, spec, cfg)
+    for i in list(range(5)) + list(range(f - 5, f)) + [f // 2]:
+        one = vt.decode_matrix_batch(llrs[i:i + 1], spec, cfg)
+        np.testing.assert_array_equal(res.bits[i], one.bits[0])
+        assert res.final_metric[i] == one.final_metric[0]
