@@ -227,3 +227,25 @@ def test_matrix_r4_optimized_large_batch():
         one = vt.decode_matrix_batch(llrs[i:i + 1], spec, cfg)
         np.testing.assert_array_equal(res.bits[i], one.bits[0])
         assert res.final_metric[i] == one.final_metric[0]
+
+
+@pytest.mark.parametrize("form", [FORMS[0], FORMS[1], FORMS[2]], ids=["K7", "K7r3", "K9"])
+def test_multi_tile_hard_decision_ties(form):
+    """Hard-decision LLRs (+-1: ties at every stage) with several tiles per CTA:
+    the tie rule holds at scale (oracle on window-aligned sub-streams)."""
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    k, gens, wpc, _ = form
+    F, V = 256, 42
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = (2 * sms * wpc + 300) * F + 11
+    q = (1 - 2 * np.random.default_rng(k + len(gens)).integers(0, 2, size=(n, len(gens)))).astype(np.int8)
+    words = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(k, gens), F, V)
+    got = np.unpackbits(words.cpu().numpy().view(np.uint8), count=n, bitorder="little")
+    sub = 60 * F
+    want = oracle.decode_stream(q[:sub], k, gens, F, V, threads=8)
+    np.testing.assert_array_equal(got[: sub - F], want[: sub - F])
+    s0 = ((n - sub) // F) * F
+    want = oracle.decode_stream(q[s0:], k, gens, F, V, threads=8)
+    np.testing.assert_array_equal(got[s0 + F:], want[F:])
