@@ -238,6 +238,8 @@ def decode_stream_device(llr_nb, spec: CodeSpec, frame_len: int, overlap: int, *
     if llr_nb.dtype != torch.int8 or llr_nb.dim() != 2 or llr_nb.shape[1] != spec.outputs_per_bit:
         raise ValueError("llr must be an int8 (N, B) CUDA tensor")
     llr_nb = llr_nb.contiguous()
+    if llr_nb.data_ptr() % 16:  # e.g. a row slice: the kernels stage 16-byte words
+        llr_nb = llr_nb.clone()
     n = int(llr_nb.shape[0])
     nwords = (n + 31) // 32
     if out is None:

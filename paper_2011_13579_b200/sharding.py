@@ -61,6 +61,9 @@ def decode_stream_sharded(llr_shard_nb, spec, n: int, frame_len: int, overlap: i
     from .decoder import _code, _ptr, _stream_ptr, _workspace
 
     code = _code(spec)
+    llr_shard_nb = llr_shard_nb.contiguous()
+    if llr_shard_nb.data_ptr() % 16:  # the kernels stage 16-byte words
+        llr_shard_nb = llr_shard_nb.clone()
     nwords = (n + 31) // 32
     if out is None:
         out = torch.zeros(nwords, dtype=torch.int32, device=llr_shard_nb.device)

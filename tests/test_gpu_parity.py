@@ -175,3 +175,15 @@ def test_kernel_variants_match_oracle(vt, code, fv, variant, monkeypatch):
     wb, wm = oracle.decode_batch(np.transpose(q[:30_000].reshape(60, 500, -1), (0, 2, 1)), k, gens)
     np.testing.assert_array_equal(bits, wb)
     np.testing.assert_array_equal(metric, wm.astype(np.float64))
+
+
+def test_device_entry_accepts_unaligned_slices(vt):
+    """A row slice of an int8 (N, B) tensor starts at any byte; the entry re-aligns it."""
+    import torch
+    spec = vt.default_spec()
+    _, q = oracle.synthetic_stream(20_001, 7, (0o171, 0o133), ebn0_db=2.0, seed=31)
+    dq = torch.from_numpy(q).cuda()
+    for off in (1, 3, 8):
+        words = vt.decode_stream_device(dq[off:], spec, 256, 42)
+        got = np.unpackbits(words.cpu().numpy().view(np.uint8), count=q.shape[0] - off, bitorder="little")
+        np.testing.assert_array_equal(got, oracle.decode_stream(q[off:], 7, (0o171, 0o133), 256, 42, threads=8))
