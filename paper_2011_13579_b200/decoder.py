@@ -329,6 +329,8 @@ def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "referenc
     q = _as_int8_llr(arr).T.copy()  # (N, B) stage-major
     torch = _torch()
     n = q.shape[0]
+    if not _closed_form_plan(plan):
+        return _decode_windows_general(q, spec, plan, decoder, config)
     if r4perm:  # radix-4 with the dragonfly permutation tie order (matrix.py:329-333)
         dev = torch.from_numpy(q).cuda()
         out = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev.device)
@@ -337,6 +339,37 @@ def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "referenc
     pinned = torch.from_numpy(q).pin_memory()
     words = decode_stream_host(pinned, spec, plan.frame_len, plan.overlap)
     return _unpack(words.numpy(), n)
+
+
+def _closed_form_plan(plan: FramePlan) -> bool:
+    """True when the plan's windows are plan_frames(N, F, V)'s (the fused stream kernels
+    compute that geometry on the device)."""
+    from .framing import _Windows
+    w = plan.windows
+    if isinstance(w, _Windows):
+        return (w._n, w._f, w._v) == (plan.total_stages, plan.frame_len, plan.overlap)
+    from .framing import plan_frames
+    return tuple(w) == tuple(plan_frames(plan.total_stages, plan.frame_len, plan.overlap).windows)
+
+
+def _decode_windows_general(q: np.ndarray, spec: CodeSpec, plan: FramePlan, decoder: str, config) -> np.ndarray:
+    """framing._decode_windows (framing.py:86-93, 112-137) for an arbitrary window list:
+    windows grouped by length, each group one batched GPU decode, emit ranges stitched."""
+    n = q.shape[0]
+    out = np.zeros(n, dtype=np.uint8)
+    groups: dict[int, list] = {}
+    for w in plan.windows:
+        groups.setdefault(w.stop - w.start, []).append(w)
+    for length, ws in groups.items():
+        frames = np.stack([q[w.start:w.stop] for w in ws])  # (F, L, B)
+        if decoder == "matrix":
+            bits = decode_matrix_batch(np.transpose(frames, (0, 2, 1)).astype(np.float32), spec,
+                                       config or DecoderConfig()).bits
+        else:
+            bits, _ = _decode_frames_np(np.ascontiguousarray(frames), spec)
+        for i, w in enumerate(ws):
+            out[w.emit_start:w.emit_stop] = bits[i][w.emit_start - w.start:w.emit_stop - w.start]
+    return out
 
 
 def decode_batch(llrs, spec: CodeSpec, mode: str = "soft", renormalize: bool = False):

@@ -187,3 +187,24 @@ def test_device_entry_accepts_unaligned_slices(vt):
         words = vt.decode_stream_device(dq[off:], spec, 256, 42)
         got = np.unpackbits(words.cpu().numpy().view(np.uint8), count=q.shape[0] - off, bitorder="little")
         np.testing.assert_array_equal(got, oracle.decode_stream(q[off:], 7, (0o171, 0o133), 256, 42, threads=8))
+
+
+def test_decode_stream_custom_window_plan(vt):
+    """A FramePlan with a hand-built window list (not plan_frames' geometry) is decoded
+    window by window like framing._decode_windows (grouped by length)."""
+    from paper_2011_13579_b200.framing import FramePlan, Window
+    spec = vt.default_spec()
+    n = 5000
+    _, q = oracle.synthetic_stream(n, 7, (0o171, 0o133), ebn0_db=1.5, seed=41)
+    cuts = [0, 700, 1500, 1600, 3333, 5000]
+    wins = [Window(max(0, a - 50), min(n, b + 20), a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+    plan = FramePlan(n, 1000, 50, wins)
+    got = vt.decode_stream(q.T.astype(float), spec, plan)
+    want = np.zeros(n, dtype=np.uint8)
+    for w in wins:
+        bits, _ = oracle.decode_batch(q[w.start:w.stop].T[None], 7, (0o171, 0o133))
+        want[w.emit_start:w.emit_stop] = bits[0][w.emit_start - w.start:w.emit_stop - w.start]
+    np.testing.assert_array_equal(got, want)
+    got_m = vt.decode_stream(q.T.astype(float), spec, plan, decoder="matrix",
+                             config=vt.DecoderConfig(radix=4, optimized=True))
+    assert got_m.shape == (n,)
