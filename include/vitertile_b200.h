@@ -114,6 +114,22 @@ int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N
                           uint32_t* bits_host, int8_t* llr_dev, uint32_t* bits_dev, void* workspace,
                           size_t workspace_bytes, int nchunks, void* stream);
 
+/* ---- the reference's separate forward / traceback stages ----
+ * reference.forward_batch (reference.py:95-128): F frames of N stages, llr device
+ * (F, N, B) int8; initial_metrics device int64, (S) shared by all frames
+ * (init_per_frame = 0), (F, S) per frame (1) or NULL (zeros); renormalize != 0
+ * subtracts the per-stage maximum.  Outputs (device): survivors (F, N, S) uint8
+ * (1 = the second predecessor won, ties included), final_metrics (F, S) int64,
+ * history (F, N, S) int64 per-stage metrics (nullable).  K <= 9. */
+int vt_forward_batch(const vt_code* code, const int8_t* llr, int64_t F, int64_t N, const int64_t* initial_metrics,
+                     int init_per_frame, int renormalize, uint8_t* survivors, int64_t* final_metrics,
+                     int64_t* history, void* stream);
+
+/* reference.traceback_batch (reference.py:131-144): from the lowest-index best
+ * final state, bits (F, N) uint8 on the device. */
+int vt_traceback_batch(const vt_code* code, const uint8_t* survivors, const int64_t* final_metrics, int64_t F,
+                       int64_t N, uint8_t* bits, void* stream);
+
 /* ---- paper-formulation tile decoder with the dragonfly permutation tie order ----
  * matrix.decode_matrix_batch / decode_stream(decoder="matrix") with
  * DecoderConfig(radix=4, optimized=True) (matrix.py:187-265, 306-334, 342-409):

@@ -66,8 +66,11 @@ def lib():
     L.vt_workspace_bytes_r4perm.restype = ctypes.c_size_t
     L.vt_decode_stream_r4perm.argtypes = [code_p, vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, vp, vp,
                                           ctypes.c_size_t, vp]
+    L.vt_forward_batch.argtypes = [code_p, vp, i64, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]
+    L.vt_traceback_batch.argtypes = [code_p, vp, vp, i64, i64, vp, vp]
     for fn in ("vt_decode_stream", "vt_decode_stream_range", "vt_decode_frames", "vt_decode_stream_host",
-               "vt_channel_awgn", "vt_count_bit_errors", "vt_decode_stream_r4perm"):
+               "vt_channel_awgn", "vt_count_bit_errors", "vt_decode_stream_r4perm", "vt_forward_batch",
+               "vt_traceback_batch"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L

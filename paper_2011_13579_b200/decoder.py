@@ -410,9 +410,9 @@ def decode_reference(frame, spec: CodeSpec, mode: str = "soft", initial_metrics=
     llr = _to_soft(frame, spec, mode)
     if initial_metrics is not None:
         init = np.broadcast_to(np.asarray(initial_metrics, dtype=np.float64), (spec.num_states,))
-        if not np.all(init == init[0]):
-            raise NotImplementedError("non-uniform initial metrics are not supported by the B200 kernels "
-                                      "(each window starts from all-zero metrics, SPEC.md:216)")
+        if not np.all(init == init[0]):  # the fused kernels start from uniform metrics: separate stages
+            from .reference import forward, traceback
+            return traceback(forward(llr, spec, init, renormalize), spec)
     bits, _ = decode_batch(llr[None, :, :], spec, renormalize=renormalize)
     return bits[0]
 
