@@ -107,3 +107,28 @@ def test_framing_penalty_matches_reference_anchor(vt):
     e_framed, e_bare = int(np.count_nonzero(framed != bits)), int(np.count_nonzero(bare != bits))
     assert e_framed <= 3
     assert 89 - 4 * math.sqrt(89) <= e_bare <= 89 + 4 * math.sqrt(89), e_bare
+
+
+@pytest.mark.parametrize("k,gens", [(7, (0o171, 0o133)), (9, (0o753, 0o561)), (3, (0o7, 0o5)),
+                                    (7, (0o133, 0o171, 0o165))])
+@pytest.mark.parametrize("flen", [37, 1023])
+def test_gpu_encoder_matches_encode_batch_exactly(vt, k, gens, flen):
+    """Noiseless channel: every LLR is +-16 exactly, i.e. the fused encoder equals
+    codes.encode_batch (zero state at every frame start) for each code and frame length."""
+    import ctypes
+    import torch
+    from paper_2011_13579_b200 import _lib
+    from paper_2011_13579_b200.decoder import _code, _ptr
+    spec = vt.CodeSpec(k, gens)
+    b = len(gens)
+    frames = 300
+    n = frames * flen
+    bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    llr = torch.zeros(((n * b + 15) // 16) * 16, dtype=torch.int8, device="cuda")
+    _lib.check(_lib.lib().vt_channel_awgn(ctypes.byref(_code(spec)), 9, 2, frames, flen, 0.0, 16.0, 0, _ptr(bits),
+                                          _ptr(llr), None))
+    torch.cuda.synchronize()
+    u = np.unpackbits(bits.cpu().numpy().view(np.uint8), count=n, bitorder="little").reshape(frames, flen)
+    coded = vt.encode_batch(u, spec).reshape(n, b)
+    q = llr.cpu().numpy()[: n * b].reshape(n, b)
+    np.testing.assert_array_equal(q, (16 * (1 - 2 * coded.astype(np.int64))).astype(np.int8))
