@@ -132,3 +132,23 @@ def test_gpu_encoder_matches_encode_batch_exactly(vt, k, gens, flen):
     coded = vt.encode_batch(u, spec).reshape(n, b)
     q = llr.cpu().numpy()[: n * b].reshape(n, b)
     np.testing.assert_array_equal(q, (16 * (1 - 2 * coded.astype(np.int64))).astype(np.int8))
+
+
+def test_matrix_decoder_points_use_the_radix4_tie_order(vt):
+    """run_point(decoder="matrix", radix-4 optimised): both random sources decode with the
+    dragonfly-permutation tie order (the numpy point equals decode_matrix_batch on the
+    same quantised frames; the GPU point runs the r4perm kernel)."""
+    from paper_2011_13579_b200 import channel as ch
+    spec = vt.default_spec()
+    cfg = vt.DecoderConfig(radix=4, optimized=True)
+    p = ch.run_point(spec, 1.0, 50_000, decoder="matrix", config=cfg, seed=8, frame_len=500, point_index=2,
+                     rng="numpy", llr_scale=2.0)  # coarse quantisation: ties
+    frames = -(-50_000 // 500)
+    data = ch.generate_bits(frames * 500, 8, 2).reshape(frames, 500)
+    y = ch.modulate_awgn(vt.encode_batch(data, spec), ch.ChannelModel(1.0, seed=8), 0.5, 2)
+    q = np.clip(np.rint(y * 2.0), -127, 127).astype(np.int8)
+    bits = vt.decode_matrix_batch(np.transpose(q, (0, 2, 1)).astype(np.float32), spec, cfg).bits
+    assert p.errors == int(np.count_nonzero(bits != data))
+    g = ch.run_point(spec, 1.0, 200_000, decoder="matrix", config=cfg, seed=8, frame_len=500, point_index=2)
+    r = ch.run_point(spec, 1.0, 200_000, seed=8, frame_len=500, point_index=2)
+    assert g.n == r.n and abs(g.ber - r.ber) < 0.1 * r.ber  # same channel samples, different tie order
