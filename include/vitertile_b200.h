@@ -130,6 +130,12 @@ int vt_forward_batch(const vt_code* code, const int8_t* llr, int64_t F, int64_t 
 int vt_traceback_batch(const vt_code* code, const uint8_t* survivors, const int64_t* final_metrics, int64_t F,
                        int64_t N, uint8_t* bits, void* stream);
 
+/* Host helper for reference-style inputs: float64 LLRs (B, N) (row b at
+ * llr + b*row_stride) -> int8 stage-major (N, B) in one multithreaded pass
+ * (nthreads <= 0: all cores).  VT_EINVAL when a value is not an integer in
+ * [-128, 127] (the reference API's float LLRs must be quantised first). */
+int vt_pack_llr_f64(const double* llr, int64_t B, int64_t N, int64_t row_stride, int8_t* out, int nthreads);
+
 /* ---- paper-formulation tile decoder with the dragonfly permutation tie order ----
  * matrix.decode_matrix_batch / decode_stream(decoder="matrix") with
  * DecoderConfig(radix=4, optimized=True) (matrix.py:187-265, 306-334, 342-409):

@@ -67,6 +67,8 @@ def lib():
     L.vt_decode_stream_r4perm.argtypes = [code_p, vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, vp, vp,
                                           ctypes.c_size_t, vp]
     L.vt_forward_batch.argtypes = [code_p, vp, i64, i64, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]
+    L.vt_pack_llr_f64.argtypes = [vp, i64, i64, i64, vp, ctypes.c_int]
+    L.vt_pack_llr_f64.restype = ctypes.c_int
     L.vt_traceback_batch.argtypes = [code_p, vp, vp, i64, i64, vp, vp]
     for fn in ("vt_decode_stream", "vt_decode_stream_range", "vt_decode_frames", "vt_decode_stream_host",
                "vt_channel_awgn", "vt_count_bit_errors", "vt_decode_stream_r4perm", "vt_forward_batch",

@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
+#include <thread>
+#include <vector>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -261,6 +264,34 @@ int vt_decode_frames(const vt_code* code, const int8_t* llr, int64_t frames, int
   if (frames < 1 || n < 1) return fail(VT_EINVAL, "need frames >= 1 and n >= 1");
   // F independent frames == a stream of frames*n stages cut with F=n, V=0
   return vt_decode_stream(code, llr, frames * n, n, 0, bits, final_metric, workspace, workspace_bytes, stream);
+}
+
+int vt_pack_llr_f64(const double* llr, int64_t B, int64_t N, int64_t row_stride, int8_t* out, int nthreads) {
+  if (!llr || !out || B < 1 || N < 0 || row_stride < N) return fail(VT_EINVAL, "bad LLR buffer geometry");
+  if (nthreads < 1) nthreads = (int)std::min<unsigned>(32u, std::max(1u, std::thread::hardware_concurrency()));
+  const int64_t per = std::max<int64_t>(1 << 16, (N + nthreads - 1) / nthreads);
+  std::atomic<int64_t> bad{-1};  // lowest offending stage seen (any), -1 if none
+  auto work = [&](int64_t t0, int64_t t1) {
+    for (int64_t t = t0; t < t1; ++t) {
+      for (int64_t b = 0; b < B; ++b) {
+        const double v = llr[b * row_stride + t];
+        if (!(v == std::rint(v)) || v < -128.0 || v > 127.0) {  // NaN fails the first test
+          int64_t e = bad.load();
+          while ((e < 0 || t < e) && !bad.compare_exchange_weak(e, t)) {}
+          return;
+        }
+        out[t * B + b] = (int8_t)v;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int64_t t0 = per; t0 < N; t0 += per) pool.emplace_back(work, t0, std::min(N, t0 + per));
+  work(0, std::min(N, per));
+  for (auto& th : pool) th.join();
+  if (bad.load() >= 0)
+    return fail(VT_EINVAL, "LLR at stage %lld is not an integer in [-128, 127] (int8-quantised LLRs; use "
+                "quantize_llr)", (long long)bad.load());
+  return VT_OK;
 }
 
 int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N, int64_t F, int64_t V,

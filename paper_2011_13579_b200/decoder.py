@@ -326,8 +326,17 @@ def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "referenc
         cfg = config or DecoderConfig()
         _, _, effective = _check_matrix_config(spec, cfg)
         r4perm = cfg.radix == 4 and cfg.optimized and effective
-    q = _as_int8_llr(arr).T.copy()  # (N, B) stage-major
     torch = _torch()
+    if arr.dtype == np.float64 and not r4perm and _closed_form_plan(plan):
+        # reference-style float LLRs: one native pass checks, converts and transposes
+        # straight into pinned memory, then the pipelined host entry
+        a64 = np.ascontiguousarray(arr)
+        n = a64.shape[1]
+        pinned = torch.empty((n, a64.shape[0]), dtype=torch.int8, pin_memory=True)
+        check(lib().vt_pack_llr_f64(a64.ctypes.data_as(ctypes.c_void_p), a64.shape[0], n, n, _ptr(pinned), 0))
+        words = decode_stream_host(pinned, spec, plan.frame_len, plan.overlap)
+        return _unpack(words.numpy(), n)
+    q = _as_int8_llr(arr).T.copy()  # (N, B) stage-major
     n = q.shape[0]
     if not _closed_form_plan(plan):
         return _decode_windows_general(q, spec, plan, decoder, config)

@@ -84,3 +84,22 @@ def test_decode_argument_validation_without_gpu():
 def test_quantizer():
     q = vt.quantize_llr(np.array([0.01, -3.0, 100.0, -100.0]), scale=16)
     np.testing.assert_array_equal(q, np.array([0, -48, 127, -127], dtype=np.int8))
+
+
+def test_pack_llr_f64_host_helper():
+    """vt_pack_llr_f64 (host, no GPU): float64 (B, N) -> int8 (N, B) in one pass; rejects
+    non-integers, NaN and out-of-range values with the lowest offending stage."""
+    import ctypes
+    L = _lib.lib()
+    rng = np.random.default_rng(0)
+    n = 300_001
+    a = rng.integers(-128, 128, size=(3, n)).astype(np.float64)
+    out = np.empty((n, 3), dtype=np.int8)
+    vp = ctypes.c_void_p
+    assert L.vt_pack_llr_f64(a.ctypes.data_as(vp), 3, n, n, out.ctypes.data_as(vp), 0) == 0
+    np.testing.assert_array_equal(out, a.T.astype(np.int8))
+    for bad, where in ((0.5, 200_000), (float("nan"), 77), (128.0, 5), (-129.0, 299_999), (float("inf"), 1)):
+        b = a.copy()
+        b[2, where] = bad
+        assert L.vt_pack_llr_f64(b.ctypes.data_as(vp), 3, n, n, out.ctypes.data_as(vp), 4) == -1
+        assert f"stage {where} " in L.vt_last_error().decode()
