@@ -72,3 +72,21 @@ def test_stream_longer_than_2_31(decoded, where):
     hi = (s1 - s0) if s1 == N else (s1 - s0) - F
     got = _bits(words, s0 + lo, s0 + hi)
     np.testing.assert_array_equal(got, want[lo:hi])
+
+
+@pytest.mark.parametrize("k,gens", [(9, (0o753, 0o561))], ids=["K9-multilane"])
+def test_stream_longer_than_2_31_other_forms(stream, k, gens):
+    """The multi-lane K=9 kernel on the same > 2^31-stage stream (the random int8 LLRs
+    are as valid for (753,561) as for (171,133)): start, 2^31 boundary and end."""
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    words = vt.decode_stream_device(stream, vt.CodeSpec(k, gens), F, V)
+    torch.cuda.synchronize()
+    for s0, s1 in ((0, SUB), (((1 << 31) // F - 32) * F, ((1 << 31) // F - 32) * F + SUB),
+                   (((N - SUB) // F) * F, N)):
+        sub = stream[s0:s1].cpu().numpy()
+        want = oracle.decode_stream(sub, k, gens, F, V, threads=8)
+        lo = 0 if s0 == 0 else F
+        hi = (s1 - s0) if s1 == N else (s1 - s0) - F
+        np.testing.assert_array_equal(_bits(words, s0 + lo, s0 + hi), want[lo:hi])
