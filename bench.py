@@ -301,13 +301,13 @@ def other_configs(torch, vt, dev, steps: int) -> list:
     cases = [("K=7 r1/3 (133,171,165)", 7, (0o133, 0o171, 0o165), 1 << 28, 256, 42),
              ("K=9 r1/2 (753,561)", 9, (0o753, 0o561), 1 << 28, 256, 42),
              ("K=9 r1/2 (753,561) V=54", 9, (0o753, 0o561), 1 << 28, 256, 54)]
-    for f in (64, 128, 256, 512, 1024):
-        cases.append((f"K=7 r1/2 sweep F={f}", 7, GENS, 1 << 26, f, 42))
+    # the headline workload through the other kernel forms (VT_KERNEL_VARIANT)
+    cases.append(("K=7 r1/2 F=256 tensor-core branch metrics (16x2tc)", 7, GENS, 1 << 28, 256, 42, "16x2tc"))
+    cases.append(("K=7 r1/2 F=256 one window per thread (s32)", 7, GENS, 1 << 28, 256, 42, "s32"))
     for lw in (16, 18, 22):  # batch sweep at F=256 (2^20 windows is the headline)
         cases.append((f"K=7 r1/2 sweep windows=2^{lw} (F=256)", 7, GENS, 256 << lw, 256, 42))
-    # the same headline code through the other kernel forms (VT_KERNEL_VARIANT)
-    cases.append(("K=7 r1/2 F=256 tensor-core branch metrics (16x2tc)", 7, GENS, 1 << 26, 256, 42, "16x2tc"))
-    cases.append(("K=7 r1/2 F=256 one window per thread (s32)", 7, GENS, 1 << 26, 256, 42, "s32"))
+    for f in (64, 128, 256, 512, 1024):  # frame-length sweep at the headline batch (2^20 windows)
+        cases.append((f"K=7 r1/2 sweep F={f} (2^20 windows)", 7, GENS, f << 20, f, 42))
     stream = torch.cuda.current_stream()
     for case in cases:
         label, k, gens, n, f, v = case[:6]
