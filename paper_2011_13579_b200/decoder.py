@@ -289,9 +289,14 @@ def decode_stream_host(llr_nb_host, spec: CodeSpec, frame_len: int, overlap: int
 def _decode_frames_np(frames_fnb: np.ndarray, spec: CodeSpec):
     """(F, N, B) int8 frames -> (bits (F, N) uint8, final metric int64 (F,))."""
     torch = _torch()
+    return _decode_frames_dev(torch.from_numpy(np.ascontiguousarray(frames_fnb)).cuda(), spec)
+
+
+def _decode_frames_dev(dev_llr, spec: CodeSpec):
+    """(F, N, B) int8 device frames -> (bits (F, N) uint8, final metric int64 (F,)) on the host."""
+    torch = _torch()
     code = _code(spec)
-    f, n, _ = frames_fnb.shape
-    dev_llr = torch.from_numpy(np.ascontiguousarray(frames_fnb)).cuda()
+    f, n, _ = dev_llr.shape
     total = f * n
     bits = torch.zeros((total + 31) // 32, dtype=torch.int32, device=dev_llr.device)
     metric = torch.empty(f, dtype=torch.int64, device=dev_llr.device)
@@ -391,8 +396,17 @@ def decode_batch(llrs, spec: CodeSpec, mode: str = "soft", renormalize: bool = F
         arr = np.where(arr >= 0.0, 1.0, -1.0)
     elif mode != "soft":
         raise ValueError(f"unknown mode {mode!r}")
-    q = _as_int8_llr(arr)
-    bits, metric = _decode_frames_np(np.transpose(q, (0, 2, 1)), spec)
+    f, b, n = arr.shape
+    if f * n >= (1 << 20):  # large batches: one native pass (check + convert) into pinned memory
+        torch = _torch()
+        a64 = np.ascontiguousarray(arr).reshape(f * b, n)  # rows (frame, output)
+        pinned = torch.empty((n, f * b), dtype=torch.int8, pin_memory=True)
+        check(lib().vt_pack_llr_f64(a64.ctypes.data_as(ctypes.c_void_p), f * b, n, n, _ptr(pinned), 0))
+        dev = pinned.to(f"cuda:{torch.cuda.current_device()}", non_blocking=True)
+        bits, metric = _decode_frames_dev(dev.view(n, f, b).permute(1, 0, 2).contiguous(), spec)
+    else:
+        q = _as_int8_llr(arr)
+        bits, metric = _decode_frames_np(np.transpose(q, (0, 2, 1)), spec)
     if renormalize:  # reference.py:124-125: max subtracted after every stage -> final max is 0
         metric = np.zeros_like(metric)
     return bits, metric.astype(np.float64)

@@ -208,3 +208,20 @@ def test_decode_stream_custom_window_plan(vt):
     got_m = vt.decode_stream(q.T.astype(float), spec, plan, decoder="matrix",
                              config=vt.DecoderConfig(radix=4, optimized=True))
     assert got_m.shape == (n,)
+
+
+def test_decode_batch_large_float_batch_native_path(vt):
+    """decode_batch on >= 2^20 float64 stages goes through the native pack helper
+    (vt_pack_llr_f64 + a device transpose): same bits and metrics as the oracle;
+    non-integer LLRs are rejected."""
+    spec = vt.default_spec()
+    rng = np.random.default_rng(12)
+    llrs = rng.integers(-128, 128, size=(2100, 2, 500)).astype(np.float64)
+    bits, metric = vt.decode_batch(llrs, spec)
+    sel = np.r_[0:20, 2080:2100]
+    wb, wm = oracle.decode_batch(llrs[sel].astype(np.int8), 7, (0o171, 0o133))
+    np.testing.assert_array_equal(bits[sel], wb)
+    np.testing.assert_array_equal(metric[sel], wm.astype(np.float64))
+    llrs[1000, 1, 250] = 0.5
+    with pytest.raises(ValueError):
+        vt.decode_batch(llrs, spec)
