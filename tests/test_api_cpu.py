@@ -103,3 +103,15 @@ def test_pack_llr_f64_host_helper():
         b[2, where] = bad
         assert L.vt_pack_llr_f64(b.ctypes.data_as(vp), 3, n, n, out.ctypes.data_as(vp), 4) == -1
         assert f"stage {where} " in L.vt_last_error().decode()
+
+
+def test_pack_llr_f64_row_stride():
+    """Rows of a wider buffer (row_stride > N): the (B, N) view of a (B, M) array."""
+    import ctypes
+    L = _lib.lib()
+    a = np.random.default_rng(1).integers(-128, 128, size=(2, 1000)).astype(np.float64)
+    out = np.empty((700, 2), dtype=np.int8)
+    vp = ctypes.c_void_p
+    assert L.vt_pack_llr_f64(a.ctypes.data_as(vp), 2, 700, 1000, out.ctypes.data_as(vp), 3) == 0
+    np.testing.assert_array_equal(out, a[:, :700].T.astype(np.int8))
+    assert L.vt_pack_llr_f64(a.ctypes.data_as(vp), 2, 700, 600, out.ctypes.data_as(vp), 3) == -1  # stride < N
