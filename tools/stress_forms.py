@@ -1,0 +1,55 @@
+"""Randomised stress of every kernel form: random frame length / overlap / stream
+length (up to multi-tile launches), LLR distributions (uniform int8, +-1 ties,
+small integers, AWGN); each decode run twice (determinism) and checked against
+the oracle on window-aligned sub-streams at both ends.
+usage: python tools/stress_forms.py [seed] [seconds]   (round 1: 1286 cases, 0 failures)"""
+import os, sys, time
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
+import numpy as np, torch
+import paper_2011_13579_b200 as vt
+from oracle import oracle
+FORMS = [(7, (0o171, 0o133), None), (7, (0o133, 0o171, 0o165), None), (9, (0o753, 0o561), None),
+         (8, (0o247, 0o371), None), (7, (0o171, 0o133), "s32"), (7, (0o171, 0o133), "16x2tc"), (5, (0o23, 0o35), None),
+         (9, (0o753, 0o561), "s32")]
+rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
+t_end = time.time() + float(sys.argv[2] if len(sys.argv) > 2 else 300)
+fails = 0; runs = 0
+while time.time() < t_end:
+    k, gens, var = FORMS[rng.integers(len(FORMS))]
+    if var: os.environ["VT_KERNEL_VARIANT"] = var
+    else: os.environ.pop("VT_KERNEL_VARIANT", None)
+    F = int(rng.choice([1, 7, 32, 33, 100, 256, 300, 777, 1024, 2048]))
+    V = int(rng.choice([0, 3, 20, 42, 64, 130, 500]))
+    nw = int(rng.integers(1, 80000)) if F >= 32 else int(rng.integers(1, 400000))
+    n = nw * F - int(rng.integers(0, F))
+    n = max(n, 1)
+    if n * len(gens) > 600_000_000: continue
+    kind = rng.integers(4)
+    if kind == 0: q = rng.integers(-128, 128, size=(n, len(gens))).astype(np.int8)
+    elif kind == 1: q = (1 - 2 * rng.integers(0, 2, size=(n, len(gens)))).astype(np.int8)
+    elif kind == 2: q = rng.integers(-3, 4, size=(n, len(gens))).astype(np.int8)
+    else:
+        _, q = oracle.synthetic_stream(n, k, gens, ebn0_db=float(rng.uniform(0, 5)), seed=int(rng.integers(1 << 16)), scale=16.0)
+    spec = vt.CodeSpec(k, gens)
+    dq = torch.from_numpy(q).cuda()
+    w1 = vt.decode_stream_device(dq, spec, F, V)
+    w2 = vt.decode_stream_device(dq, spec, F, V)
+    det = bool(torch.equal(w1, w2))
+    got = np.unpackbits(w1.cpu().numpy().view(np.uint8), count=n, bitorder="little")
+    m = V // F + 2
+    sub = min(n, (m + 30) * F)
+    ok = True
+    if sub == n:
+        want = oracle.decode_stream(q, k, gens, F, V, threads=16)
+        ok = np.array_equal(got, want)
+    else:
+        want = oracle.decode_stream(q[:sub], k, gens, F, V, threads=16)
+        ok = np.array_equal(got[: sub - m * F], want[: sub - m * F])
+        s0 = ((n - sub) // F) * F
+        want = oracle.decode_stream(q[s0:], k, gens, F, V, threads=16)
+        ok = ok and np.array_equal(got[s0 + m * F:], want[m * F:])
+    runs += 1
+    if not (ok and det):
+        fails += 1
+        print("FAIL", k, oct(gens[0]), var, "F", F, "V", V, "n", n, "kind", kind, "det", det, "ok", ok, flush=True)
+print("runs", runs, "fails", fails)
