@@ -249,3 +249,29 @@ def test_multi_tile_hard_decision_ties(form):
     s0 = ((n - sub) // F) * F
     want = oracle.decode_stream(q[s0:], k, gens, F, V, threads=8)
     np.testing.assert_array_equal(got[s0 + F:], want[F:])
+
+
+@pytest.mark.parametrize("form", [FORMS[0], FORMS[2], FORMS[5], FORMS[1]], ids=["K7", "K9", "K7-tc", "K7r3"])
+def test_multi_tile_padding_skip_does_not_overrun_traceback(form, monkeypatch):
+    """V = 0 (no warm-up groups) with a short last window: the threads of the last,
+    nearly empty tile decode the short window (or a dummy copy of it) and could skip
+    its leading zero padding; the skip is capped so their history stores never
+    overtake the previous tile's traceback fetches (found by tools/stress_forms.py:
+    whole windows garbled)."""
+    import torch
+
+    import paper_2011_13579_b200 as vt
+    k, gens, wpc, variant = form
+    if variant:
+        monkeypatch.setenv("VT_KERNEL_VARIANT", variant)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    F, V = 300, 0
+    nw = 2 * sms * wpc + 16  # the last tile holds 16 windows, the last one 130 stages long
+    n = (nw - 1) * F + 130
+    q = np.random.default_rng(k).integers(-3, 4, size=(n, len(gens))).astype(np.int8)
+    words = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(k, gens), F, V)
+    got = np.unpackbits(words.cpu().numpy().view(np.uint8), count=n, bitorder="little")
+    for w in list(range(0, 2 * wpc, 7)) + [nw - 1]:
+        s, e = w * F, min(n, (w + 1) * F)
+        wb, _ = oracle.decode_batch(np.ascontiguousarray(q[s:e].T[None]), k, gens)
+        np.testing.assert_array_equal(got[s:e], wb[0], err_msg=f"window {w}")
