@@ -2,7 +2,7 @@
 length (up to multi-tile launches), LLR distributions (uniform int8, +-1 ties,
 small integers, AWGN); each decode run twice (determinism) and checked against
 the oracle on window-aligned sub-streams at both ends.
-usage: python tools/stress_forms.py [seed] [seconds]   (round 1: 3317 cases over two seeds, 0 failures)"""
+usage: python tools/stress_forms.py [seed] [seconds]   (round 1: found one bug (padding-skip overrun, fixed); 2767 cases after the fix, 0 failures)"""
 import os, sys, time
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import numpy as np, torch
