@@ -536,15 +536,13 @@ class Gen16:
             e(f"    uint32_t curA[{self.NWB}], curB[{self.NWB}];  // this body's LLR words (realigned per body)")
         elif not self.tc:
             e("    uint32_t curA[NWC], curB[NWC];")
-        e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole bodies of it -- at most")
-        e(f"    // b_lo groups' worth: the stores of this tile run {self.GPB}*it0 groups ahead of its group-end")
-        e("    // count, and the previous tile's traceback must have fetched a slot position before this tile")
-        e("    // overwrites it (skipping more would overwrite history the traceback still needs)")
-        skip = f"min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, (int64_t)min({self.CHB}, a.b_lo / {self.GPB}))"
+        e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole bodies of it")
         if self.tc:  # warp-uniform: tcgen05.ld is .sync.aligned, so every lane must run the same bodies
-            e(f"    const int it0 = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned){skip});")
+            e(f"    const int it0 = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)min(min(max(gA.s - gA.g0, (int64_t)0), "
+              f"max(gB.s - gB.g0, (int64_t)0)) / {P}, (int64_t){self.CHB}));")
         else:
-            e(f"    const int it0 = (int){skip};")
+            e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
+              f"(int64_t){self.CHB});")
         e("    int it_start = it0;")
         if self.tc:
             e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")

@@ -415,10 +415,8 @@ class Gen16M(Gen16):
         if self.fm:
             e(f"    int64_t offA = {-self.Sb}, offB = {-self.Sb}, pendA = 0, pendB = 0;")
         e(f"    uint32_t curA[{self.NWB}], curB[{self.NWB}];")
-        # padding bodies skipped: at most b_lo groups' worth (see Gen16: the previous tile's
-        # traceback must fetch a slot position before this tile's stores overwrite it)
         e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
-          f"(int64_t)min({self.CHB}, a.b_lo / {self.GPB}));")
+          f"(int64_t){self.CHB});")
         e("    int it_start = it0;")
         e("    __syncwarp(pm);  // the previous tile's rows are consumed")
         e(f"    vt::stage_row_part<NL, {T}>(llrA(0), a.llr, buf_bytes, oA, fastA, t);")
