@@ -22,7 +22,10 @@
  * Conventions (all calls):
  *   - Plain pointers and sizes; no allocation inside a call (the caller passes
  *     the workspace sized by vt_workspace_bytes).  Calls are reentrant and
- *     thread-safe (no mutable globals); errors are reported per thread.
+ *     thread-safe; errors are reported per thread.  The only shared state is
+ *     append-only: per-(kernel, device) launch facts computed on first use and
+ *     the kernels of loaded code modules (vt_load_code_module), both published
+ *     with atomics.
  *   - LLRs are int8, stage-major (N, B): element (t, b) at llr[t*B + b], the
  *     layout of the reference CLI's LLR files (cli.py:136-140).  Positive LLR
  *     means the coded bit is more likely 0 (reference.py:28).
@@ -76,6 +79,30 @@ int vt_version(void);
 /* 1 if a compiled sm_100a kernel exists for this code, else 0. */
 int vt_code_supported(const vt_code* code);
 
+/* ---- code modules: kernels generated and compiled at run time for codes the
+ * library was not built with (the reference decodes any CodeSpec,
+ * codes.py:52-107; cli.py:85-90).  paper_2011_13579_b200/jit.py generates the
+ * same kernel forms as the build for the new (K, generators), compiles them
+ * for sm_100a into a shared library exporting
+ *     int vtm_kernels(vt_module_kernel* out, int max);
+ * and registers it here.  Module kernels launch through the module (its own
+ * CUDA runtime registration); everything else is shared with built-in codes. */
+#define VT_MODULE_VERSION 1
+typedef int (*vt_module_launch_fn)(const void* stream_args, long long grid, int no_final_metric, void* stream);
+typedef int (*vt_module_prepare_fn)(int* ctas_per_sm);
+typedef struct vt_module_kernel {
+  int32_t version;                 /* VT_MODULE_VERSION */
+  int32_t K, B, T, WPT, SL, CH, BL, SQ, body;
+  uint32_t gens[VT_MAX_OUTPUTS];
+  int32_t smem, tc, nt, has_nofm;
+  vt_module_launch_fn launch;      /* returns a cudaError_t value */
+  vt_module_prepare_fn prepare;    /* shared-memory opt-in + occupancy; returns a cudaError_t value */
+} vt_module_kernel;
+
+/* Load a code module and register its kernels; returns the number of kernels
+ * registered (> 0) or a VT_E* code.  Registered codes stay for the process. */
+int vt_load_code_module(const char* path);
+
 /* Message describing the last error on the calling thread ("" if none). */
 const char* vt_last_error(void);
 
@@ -113,6 +140,31 @@ int vt_decode_frames(const vt_code* code, const int8_t* llr, int64_t frames, int
 int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N, int64_t F, int64_t V,
                           uint32_t* bits_host, int8_t* llr_dev, uint32_t* bits_dev, void* workspace,
                           size_t workspace_bytes, int nchunks, void* stream);
+
+/* Workspace bytes for vt_decode_stream_host over windows [w0, w1) in nchunks
+ * pipelined pieces (the maximum over the pieces). */
+size_t vt_workspace_bytes_host(const vt_code* code, int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1,
+                               int nchunks);
+
+/* Shard g of ndev (frames shard with no exchange): out[0..1]
+ * = window range [w0, w1), out[2..3] = the stage range [st0, st1) its
+ * windows read (V-stage halos; st0 a multiple of 16). */
+int vt_shard_range(int64_t N, int64_t F, int64_t V, int ndev, int g, int64_t out[4]);
+
+/* decode_stream with HOST buffers over several devices (framing.decode_stream
+ * with workers, framing.py:121-135: the reference fans one stream's windows
+ * over threads; here over GPUs).  Shard g (vt_shard_range) runs on
+ * devices[g] on its own host thread and stream, pipelined like
+ * vt_decode_stream_host: llr_dev[g] holds its stages [st0, st1) (>= (st1 -
+ * st0) * B bytes), bits_dev[g] >= ceil(N/32) words, workspace[g] >=
+ * vt_workspace_bytes_host(code, N, F, V, w0, w1, nchunks) on that device.
+ * Each shard copies the words only it writes straight into bits_host; words
+ * two shards share are OR-merged on the host.  A device may appear more than
+ * once (separate streams).  Synchronous on return. */
+int vt_decode_stream_host_multi(const vt_code* code, const int8_t* llr_host, int64_t N, int64_t F, int64_t V,
+                                uint32_t* bits_host, int ndev, const int* devices, int8_t* const* llr_dev,
+                                uint32_t* const* bits_dev, void* const* workspace, const size_t* workspace_bytes,
+                                int nchunks);
 
 /* ---- the reference's separate forward / traceback stages ----
  * reference.forward_batch (reference.py:95-128): F frames of N stages, llr device

@@ -34,6 +34,7 @@ from .decoder import (
     workspace_bytes,
 )
 from . import fileio  # noqa: F401  (cli.py file formats)
+from . import sharding  # noqa: F401  (multi-GPU window shards)
 from .framing import DEFAULT_FRAME_LEN, DEFAULT_OVERLAP, FramePlan, Window, plan_frames
 
 __all__ = [

@@ -51,6 +51,8 @@ def lib():
     L.vt_code_supported.argtypes = [code_p]
     L.vt_code_supported.restype = ctypes.c_int
     L.vt_last_error.restype = ctypes.c_char_p
+    L.vt_load_code_module.argtypes = [ctypes.c_char_p]
+    L.vt_load_code_module.restype = ctypes.c_int
     L.vt_workspace_bytes.argtypes = [code_p, i64, i64, i64, i64, i64]
     L.vt_workspace_bytes.restype = ctypes.c_size_t
     L.vt_decode_stream.argtypes = [code_p, vp, i64, i64, i64, vp, vp, vp, ctypes.c_size_t, vp]
@@ -59,6 +61,11 @@ def lib():
     L.vt_decode_frames.argtypes = [code_p, vp, i64, i64, vp, vp, vp, ctypes.c_size_t, vp]
     L.vt_decode_stream_host.argtypes = [code_p, vp, i64, i64, i64, vp, vp, vp, vp, ctypes.c_size_t,
                                         ctypes.c_int, vp]
+    L.vt_workspace_bytes_host.argtypes = [code_p, i64, i64, i64, i64, i64, ctypes.c_int]
+    L.vt_workspace_bytes_host.restype = ctypes.c_size_t
+    L.vt_shard_range.argtypes = [i64, i64, i64, ctypes.c_int, ctypes.c_int, p(i64)]
+    L.vt_decode_stream_host_multi.argtypes = [code_p, vp, i64, i64, i64, vp, ctypes.c_int, p(ctypes.c_int), p(vp),
+                                              p(vp), p(vp), p(ctypes.c_size_t), ctypes.c_int]
     L.vt_channel_awgn.argtypes = [code_p, ctypes.c_uint64, ctypes.c_uint32, i64, i64, ctypes.c_float, ctypes.c_float,
                                   ctypes.c_int, vp, vp, vp]
     L.vt_count_bit_errors.argtypes = [vp, vp, i64, vp, vp]
@@ -70,7 +77,7 @@ def lib():
     L.vt_pack_llr_f64.argtypes = [vp, i64, i64, i64, vp, ctypes.c_int]
     L.vt_pack_llr_f64.restype = ctypes.c_int
     L.vt_traceback_batch.argtypes = [code_p, vp, vp, i64, i64, vp, vp]
-    for fn in ("vt_decode_stream", "vt_decode_stream_range", "vt_decode_frames", "vt_decode_stream_host",
+    for fn in ("vt_shard_range", "vt_decode_stream_host_multi", "vt_decode_stream", "vt_decode_stream_range", "vt_decode_frames", "vt_decode_stream_host",
                "vt_channel_awgn", "vt_count_bit_errors", "vt_decode_stream_r4perm", "vt_forward_batch",
                "vt_traceback_batch"):
         getattr(L, fn).restype = ctypes.c_int

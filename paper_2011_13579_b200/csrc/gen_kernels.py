@@ -376,82 +376,82 @@ def _gen16_supported(name: str, K: int, gens: tuple[int, ...]) -> bool:
     return Gen16(name, K, gens).supported
 
 
+REGISTRY_HEADER = [
+    "// GENERATED by gen_kernels.py -- kernel registry:",
+    "// VT_KERNEL(fn, fn without final metrics or nullptr, dynamic smem bytes, tensor-core BM, threads per CTA, K, B, "
+    "lanes/window T, windows/thread, SL, chunk CH, history group BL, uint4/group SQ, body stages, {gens})",
+    "",
+]
+
+
+def code_units(name: str, K: int, gens: tuple[int, ...]) -> list[tuple[str, str, list[str], list[str]]]:
+    """Every kernel form generated for one code: (file name, CUDA source, declarations,
+    registry lines).  Used by the build (STANDARD_CODES) and by the runtime code JIT
+    (paper_2011_13579_b200/jit.py), so both produce the same kernels."""
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    if here not in sys.path:
+        sys.path.insert(0, here)
+    units = []
+    gl = ", ".join(f"{x}u" for x in gens)
+    T = threads_per_window(K)
+    g = Gen(name, K, gens, T)
+    units.append((f"vtk_{name}.cu", g.kernel(),
+                  [f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);'],
+                  [f"VT_KERNEL(vtk_{name}, nullptr, 0, 0, {NT}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, "
+                   f"{g.SQ}, 0, {{{gl}}})"]))
+    lanes = T if K in (8, 9) else 0  # (K=7 over 2 lanes measured 97.6 vs 165 Gbps: DESIGN §9b)
+    if lanes:  # packed 16x2 variant over T lanes per window pair
+        from gen_kernels16m import Gen16M
+        gm = Gen16M(name, K, gens, lanes)
+        # the host's padding-skip hazard check (vt_capi.cu launch_grid) uses the body length
+        assert gm.CH % gm.P == 0 and gm.P % gm.L == 0
+        units.append((f"vtk16m_{name}.cu", gm.kernel(),
+                      [f'extern "C" __global__ void vtk16m_{name}(const vt::StreamArgs a);',
+                       f'extern "C" __global__ void vtk16mnf_{name}(const vt::StreamArgs a);'],
+                      [f"VT_KERNEL(vtk16m_{name}, &vtk16mnf_{name}, {gm.SMEM}, 0, 128, {K}, {len(gens)}, {lanes}, 2, "
+                       f"{gm.SL}, {gm.CH}, {gm.L}, {gm.SQ}, {gm.P}, {{{gl}}})"]))
+    if K == 7 and _gen16_supported(name, K, gens):  # packed 16x2 variant: two windows per thread
+        import gen_kernels16
+        from gen_kernels16 import Gen16
+        g16 = Gen16(name, K, gens)
+        if g16.cheap and g16.B == 2 and gen_kernels16.NT == 128:  # tensor-core branch-metric variant (VT_KERNEL_VARIANT=16x2tc)
+            gtc = Gen16(name, K, gens, tc=True)
+            units.append((f"vtk16tc_{name}.cu", gtc.kernel(),
+                          [f'extern "C" __global__ void vtk16tc_{name}(const vt::StreamArgs a);',
+                           f'extern "C" __global__ void vtk16tcnf_{name}(const vt::StreamArgs a);'],
+                          [f"VT_KERNEL(vtk16tc_{name}, &vtk16tcnf_{name}, {gtc.SMEM}, 1, 128, {K}, {len(gens)}, 1, 2, "
+                           f"{gtc.S}, {gtc.CH}, {gtc.L}, {gtc.S // 16}, {gtc.P}, {{{gl}}})"]))
+        units.append((f"vtk16_{name}.cu", g16.kernel(),
+                      [f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a);',
+                       f'extern "C" __global__ void vtk16nf_{name}(const vt::StreamArgs a);'],
+                      [f"VT_KERNEL(vtk16_{name}, &vtk16nf_{name}, {g16.SMEM}, 0, {gen_kernels16.NT}, {K}, {len(gens)}, "
+                       f"1, 2, {g16.S}, {g16.CH}, {g16.L}, {g16.S // 16}, {g16.P}, {{{gl}}})"]))
+    return units
+
+
+def _write_if_changed(path: str, text: str) -> None:
+    if not os.path.exists(path) or open(path).read() != text:
+        with open(path, "w") as fh:
+            fh.write(text)
+
+
 def generate(outdir: str, codes: dict | None = None) -> list[str]:
     codes = codes or STANDARD_CODES
     os.makedirs(outdir, exist_ok=True)
     files = []
-    reg = ["// GENERATED by gen_kernels.py -- kernel registry:",
-           "// VT_KERNEL(fn, fn without final metrics or nullptr, dynamic smem bytes, tensor-core BM, threads per CTA, K, B, lanes/window T, windows/thread, SL, chunk CH, history group BL, uint4/group SQ, {gens})",
-           ""]
+    reg = list(REGISTRY_HEADER)
     decl = ["// GENERATED by gen_kernels.py -- kernel declarations", '#include "../vt_common.cuh"', ""]
     for name, (K, polys) in codes.items():
         gens = tuple(int(p, 8) for p in polys)
-        T = threads_per_window(K)
-        g = Gen(name, K, gens, T)
-        src = g.kernel()
-        path = os.path.join(outdir, f"vtk_{name}.cu")
-        if not os.path.exists(path) or open(path).read() != src:
-            with open(path, "w") as fh:
-                fh.write(src)
-        files.append(path)
-        gl = ", ".join(f"{x}u" for x in gens)
-        decl.append(f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);')
-        reg.append(f"VT_KERNEL(vtk_{name}, nullptr, 0, 0, {NT}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, {g.SQ}, {{{gl}}})")
-        lanes = T if K in (8, 9) else 0  # (K=7 over 2 lanes measured 97.6 vs 165 Gbps: DESIGN §9b)
-        if lanes:  # packed 16x2 variant over T lanes per window pair
-            import sys
-            here = os.path.dirname(os.path.abspath(__file__))
-            if here not in sys.path:
-                sys.path.insert(0, here)
-            from gen_kernels16m import Gen16M
-            gm = Gen16M(name, K, gens, lanes)
-            srcm = gm.kernel()
-            pathm = os.path.join(outdir, f"vtk16m_{name}.cu")
-            if not os.path.exists(pathm) or open(pathm).read() != srcm:
-                with open(pathm, "w") as fh:
-                    fh.write(srcm)
-            files.append(pathm)
-            decl.append(f'extern "C" __global__ void vtk16m_{name}(const vt::StreamArgs a);')
-            decl.append(f'extern "C" __global__ void vtk16mnf_{name}(const vt::StreamArgs a);')
-            reg.append(f"VT_KERNEL(vtk16m_{name}, &vtk16mnf_{name}, {gm.SMEM}, 0, 128, {K}, {len(gens)}, {lanes}, 2, "
-                       f"{gm.SL}, {gm.CH}, {gm.L}, {gm.SQ}, {{{gl}}})")
-        if K == 7 and _gen16_supported(name, K, gens):  # packed 16x2 variant: two windows per thread
-            import sys
-            here = os.path.dirname(os.path.abspath(__file__))
-            if here not in sys.path:
-                sys.path.insert(0, here)
-            from gen_kernels16 import Gen16
-            g16 = Gen16(name, K, gens)
-            src16 = g16.kernel()
-            path16 = os.path.join(outdir, f"vtk16_{name}.cu")
-            if not os.path.exists(path16) or open(path16).read() != src16:
-                with open(path16, "w") as fh:
-                    fh.write(src16)
-            files.append(path16)
-            decl.append(f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a);')
-            decl.append(f'extern "C" __global__ void vtk16nf_{name}(const vt::StreamArgs a);')
-            import gen_kernels16
-            if g16.cheap and g16.B == 2 and gen_kernels16.NT == 128:  # tensor-core branch-metric variant (VT_KERNEL_VARIANT=16x2tc)
-                gtc = Gen16(name, K, gens, tc=True)
-                srctc = gtc.kernel()
-                pathtc = os.path.join(outdir, f"vtk16tc_{name}.cu")
-                if not os.path.exists(pathtc) or open(pathtc).read() != srctc:
-                    with open(pathtc, "w") as fh:
-                        fh.write(srctc)
-                files.append(pathtc)
-                decl.append(f'extern "C" __global__ void vtk16tc_{name}(const vt::StreamArgs a);')
-                decl.append(f'extern "C" __global__ void vtk16tcnf_{name}(const vt::StreamArgs a);')
-                reg.append(f"VT_KERNEL(vtk16tc_{name}, &vtk16tcnf_{name}, {gtc.SMEM}, 1, 128, {K}, {len(gens)}, 1, 2, "
-                           f"{gtc.S}, {gtc.CH}, {gtc.L}, {gtc.S // 16}, {{{gl}}})")
-            import gen_kernels16
-            reg.append(f"VT_KERNEL(vtk16_{name}, &vtk16nf_{name}, {g16.SMEM}, 0, {gen_kernels16.NT}, {K}, {len(gens)}, 1, 2, {g16.S}, {g16.CH}, {g16.L}, "
-                       f"{g16.S // 16}, {{{gl}}})")
+        for fname, src, d, r in code_units(name, K, gens):
+            path = os.path.join(outdir, fname)
+            _write_if_changed(path, src)
+            files.append(path)
+            decl.extend(d)
+            reg.extend(r)
     for fname, lines in (("registry.inc", reg), ("registry_decl.inc", decl)):
-        rpath = os.path.join(outdir, fname)
-        text = "\n".join(lines) + "\n"
-        if not os.path.exists(rpath) or open(rpath).read() != text:
-            with open(rpath, "w") as fh:
-                fh.write(text)
+        _write_if_changed(os.path.join(outdir, fname), "\n".join(lines) + "\n")
     for stale in set(os.listdir(outdir)) - {os.path.basename(f) for f in files}:  # kernels no longer generated
         if stale.endswith(".cu"):
             os.remove(os.path.join(outdir, stale))

@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <dlfcn.h>
+#include <mutex>
+#include <string>
 #include <cmath>
 #include <thread>
 #include <vector>
@@ -58,16 +61,22 @@ Geometry geometry(int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1, int C
 // ---------------------------------------------------------------------------
 struct KernelEntry {
   int K, B, T, WPT, SL, CH, BL, SQ;
+  int body;  // stages per loop body of the 16x2 forms (the unit of the leading-padding skip); 0 for s32
   uint32_t gens[VT_MAX_OUTPUTS];
   const void* fn;
   const void* fn_nofm;  // variant without final-metric bookkeeping (nullptr: use fn)
   int smem;             // dynamic shared memory bytes per CTA
   int tc;               // 1: tensor-core branch-metric variant (opt-in)
   int nt;               // threads per CTA
+  // kernels of a runtime-loaded code module (vt_load_code_module) launch through the module,
+  // which carries its own CUDA runtime registration of them
+  vt_module_launch_fn launch;
+  vt_module_prepare_fn prepare;
 };
 
-#define VT_KERNEL(fn_, fnnf_, smem_, tc_, nt_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, ...) \
-  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, __VA_ARGS__, (const void*)&fn_, (const void*)(fnnf_), smem_, tc_, nt_},
+#define VT_KERNEL(fn_, fnnf_, smem_, tc_, nt_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, BODY_, ...) \
+  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, BODY_, __VA_ARGS__, (const void*)&fn_, (const void*)(fnnf_), smem_, tc_, nt_, \
+   nullptr, nullptr},
 }  // namespace
 #include "gen/registry_decl.inc"
 namespace {
@@ -79,6 +88,13 @@ const KernelEntry* registry(int* n) {
   *n = (int)(sizeof(table) / sizeof(table[0]));
   return table;
 }
+
+// Kernels of runtime-loaded code modules (vt_load_code_module): appended under a lock,
+// published by the release store of g_ndyn, never removed (entries stay valid).
+constexpr int kMaxDyn = 64;
+KernelEntry g_dyn[kMaxDyn];
+std::atomic<int> g_ndyn{0};
+std::mutex g_dyn_mu;
 
 // Kernel variant: "16x2" (two windows per thread -- per group of 2/4 lanes for K=8/9 --
 // in packed 16-bit halves), "s32" (one window per thread, 32-bit metrics) or "16x2tc"
@@ -104,15 +120,26 @@ const KernelEntry* find(const vt_code* c) {
   const char* env = getenv("VT_KERNEL_VARIANT");
   int n;
   const KernelEntry* t = registry(&n);
+  const int nd = g_ndyn.load(std::memory_order_acquire);
   const KernelEntry* best = nullptr;
-  for (int i = 0; i < n; ++i) {
-    if (t[i].K != c->K || t[i].B != c->B) continue;
+  for (int i = 0; i < n + nd; ++i) {
+    const KernelEntry* e = i < n ? &t[i] : &g_dyn[i - n];
+    if (e->K != c->K || e->B != c->B) continue;
     bool same = true;
-    for (int b = 0; b < c->B; ++b) same = same && t[i].gens[b] == c->gens[b];
+    for (int b = 0; b < c->B; ++b) same = same && e->gens[b] == c->gens[b];
     if (!same) continue;
-    if (!best || variant_rank(&t[i], env) < variant_rank(best, env)) best = &t[i];
+    if (!best || variant_rank(e, env) < variant_rank(best, env)) best = e;
   }
   return best;
+}
+
+// index of an entry in [static table, dynamic table] (per-entry launch caches)
+int entry_index(const KernelEntry* k) {
+  int n = 0;
+  const KernelEntry* t = registry(&n);
+  if (k >= t && k < t + n) return (int)(k - t);
+  if (k >= g_dyn && k < g_dyn + kMaxDyn) return n + (int)(k - g_dyn);
+  return -1;
 }
 
 int validate(const vt_code* c) {
@@ -127,7 +154,7 @@ int validate(const vt_code* c) {
 // Per (kernel entry, device) launch facts, computed once: the dynamic shared memory
 // opt-in (cudaFuncSetAttribute) and the CTA capacity sms * occupancy.  Small calls
 // (one frame) are host-bound, so these stay off the per-call path.
-constexpr int kMaxEntries = 64, kMaxDevices = 64;
+constexpr int kMaxEntries = 128, kMaxDevices = 64;
 std::atomic<int> g_cap[kMaxEntries][kMaxDevices];  // 0: not yet computed
 
 int current_device() {
@@ -136,34 +163,36 @@ int current_device() {
   return dev;
 }
 
-// opt the kernels into their dynamic shared memory (above the 48 KB default); idempotent
-void prepare(const KernelEntry* k) {
+// opt the kernels into their dynamic shared memory (above the 48 KB default); idempotent.
+// Returns the CTAs per SM the kernel can hold.
+int prepare(const KernelEntry* k) {
+  int occ = 1;
+  if (k->prepare) {
+    if (k->prepare(&occ) != 0 || occ < 1) occ = 1;
+    return occ;
+  }
   if (k->smem > 0) {
     cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem);
     if (k->fn_nofm) cudaFuncSetAttribute(k->fn_nofm, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem);
   }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->nt, k->smem) != cudaSuccess || occ < 1) occ = 1;
+  return occ;
 }
 
 // CTAs that run concurrently on the device (prepares the kernel on first use per device)
 int64_t cta_capacity(const KernelEntry* k) {
   const char* env = getenv("VT_CTAS_PER_SM");
-  int n = 0;
-  const int idx = (int)(k - registry(&n));
+  const int idx = entry_index(k);
   const int dev = current_device();
   const bool cacheable = !(env && atoi(env) > 0) && idx >= 0 && idx < kMaxEntries && dev < kMaxDevices;
   if (cacheable) {
     const int c = g_cap[idx][dev].load(std::memory_order_acquire);
     if (c > 0) return c;
   }
-  prepare(k);
+  int occ = prepare(k);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int occ = 1;
-  if (env && atoi(env) > 0) {
-    occ = atoi(env);
-  } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->nt, k->smem) != cudaSuccess || occ < 1) {
-    occ = 1;
-  }
+  if (env && atoi(env) > 0) occ = atoi(env);
   const int cap = sms * std::min(occ, 4);
   if (cacheable) g_cap[idx][dev].store(cap, std::memory_order_release);
   return cap;
@@ -181,30 +210,72 @@ int64_t window_len(int64_t N, int64_t F, int64_t V, int64_t w) {
   return std::min(N, e1 + V) - std::max<int64_t>(0, e0 - V);
 }
 
-// Grid of a launch.  The 16x2 kernels trace tile i back while they run tile i+1 forward
-// and skip up to CHB bodies of leading zero padding per window; a skip of more than
-// b_lo groups would let tile i+1's history stores overtake tile i's traceback fetches
-// (gen_kernels16.py).  Windows shorter than F + 2V (a short last window, V = 0) can
-// need such a skip: those launches run one tile per CTA, so no CTA decodes a tile
-// after another.  The kernels themselves stay unchanged (a runtime cap on the skip
-// measured 2.6% slower on the headline).
-int64_t launch_grid(const KernelEntry* k, const Geometry& g, int64_t N, int64_t F, int64_t V, int64_t w0,
-                    int64_t w1) {
-  int64_t grid = grid_for(k, g.nwin);
-  if (k->WPT > 1) {
-    const int64_t lmin = std::min(window_len(N, F, V, w0), window_len(N, F, V, w1 - 1));
-    const int body = 2 * k->BL, chb = k->CH / body;  // 2 history groups per body
-    const int64_t skip = std::min<int64_t>(chb, std::max<int64_t>(0, (int64_t)k->CH * g.nc - lmin) / body);
-    if (2 * skip > g.b_lo) {
-      const int64_t wpc = (int64_t)k->nt * k->WPT / k->T;
-      grid = (g.nwin + wpc - 1) / wpc;
-    }
-  }
-  return grid;
+// Leading-padding hazard.  The 16x2 kernels trace tile i back while they run tile i+1
+// forward and skip up to CH/body bodies of leading zero padding per window; a skip of more
+// than b_lo history groups would let tile i+1's history stores overtake tile i's traceback
+// fetches (gen_kernels16.py).  Windows at least min(N, F + V) long never need such a skip
+// (b_lo is sized by that length), so only a suffix of short tail windows can (the window
+// length is non-increasing over the stream tail: a short last window, V = 0).
+bool skip_hazard(const KernelEntry* k, const Geometry& g, int64_t N, int64_t F, int64_t V, int64_t w) {
+  if (k->WPT <= 1 || k->body <= 0) return false;
+  const int chb = k->CH / k->body, gpb = k->body / k->BL;
+  const int64_t skip = std::min<int64_t>(chb, std::max<int64_t>(0, (int64_t)k->CH * g.nc - window_len(N, F, V, w)) /
+                                                  k->body);
+  return skip * gpb > g.b_lo;
+}
+
+// First window of the hazardous suffix of [w0, w1) (w1 when there is none).
+int64_t hazard_start(const KernelEntry* k, const Geometry& g, int64_t N, int64_t F, int64_t V, int64_t w0,
+                     int64_t w1) {
+  int64_t wh = w1;
+  while (wh > w0 && skip_hazard(k, g, N, F, V, wh - 1)) --wh;
+  return wh;
+}
+
+// One launch = the persistent grid over [w0, wh) and, when the range ends in hazardous short
+// windows, a second launch over [wh, w1) with one tile per CTA (no CTA decodes a tile after
+// another there).  The kernels stay unchanged (a runtime cap on the skip measured 2.6% slower
+// on the headline).  Scratch is reused by the second launch (stream order).
+struct LaunchPlan {
+  int64_t wh;          // split point
+  int64_t grid_main;   // CTAs of [w0, wh) (0: empty)
+  int64_t grid_tail;   // CTAs of [wh, w1) (0: empty)
+};
+
+LaunchPlan plan_launch(const KernelEntry* k, const Geometry& g, int64_t N, int64_t F, int64_t V, int64_t w0,
+                       int64_t w1) {
+  LaunchPlan p;
+  p.wh = hazard_start(k, g, N, F, V, w0, w1);
+  const int64_t wpc = (int64_t)k->nt * k->WPT / k->T;  // windows per CTA tile
+  p.grid_main = p.wh > w0 ? grid_for(k, p.wh - w0) : 0;
+  p.grid_tail = w1 > p.wh ? (w1 - p.wh + wpc - 1) / wpc : 0;
+  return p;
 }
 
 size_t scratch_bytes(const KernelEntry* k, const Geometry& g, int64_t grid) {
   return (size_t)grid * g.nbs * k->SQ * k->nt * sizeof(uint4);
+}
+
+size_t plan_scratch(const KernelEntry* k, const Geometry& g, const LaunchPlan& p) {
+  return scratch_bytes(k, g, std::max(p.grid_main, p.grid_tail));
+}
+
+int launch(const KernelEntry* k, vt::StreamArgs a, int64_t w0, int64_t w1, int64_t grid, void* stream) {
+  if (w1 <= w0 || grid <= 0) return VT_OK;
+  if (a.final_metric) a.final_metric += (w0 - a.w0);
+  a.w0 = w0;
+  a.w1 = w1;
+  const bool nofm = a.final_metric == nullptr && k->fn_nofm;
+  if (k->launch) {
+    const int e = k->launch(&a, (long long)grid, nofm ? 1 : 0, stream);
+    if (e != 0) return cuda_fail((cudaError_t)e, "kernel launch (code module)");
+    return VT_OK;
+  }
+  void* args[] = {&a};
+  const void* fn = nofm ? k->fn_nofm : k->fn;
+  cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(k->nt), args, (size_t)k->smem, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return VT_OK;
 }
 
 }  // namespace
@@ -217,11 +288,43 @@ const char* vt_last_error(void) { return g_err; }
 
 int vt_code_supported(const vt_code* code) { return find(code) != nullptr ? 1 : 0; }
 
+int vt_load_code_module(const char* path) {
+  g_err[0] = 0;
+  if (!path) return fail(VT_EINVAL, "module path is NULL");
+  void* h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+  if (!h) return fail(VT_EINVAL, "cannot load code module %s: %s", path, dlerror());
+  auto entries = reinterpret_cast<int (*)(vt_module_kernel*, int)>(dlsym(h, "vtm_kernels"));
+  if (!entries) return fail(VT_EINVAL, "%s does not export vtm_kernels", path);
+  vt_module_kernel mk[16];
+  const int n = entries(mk, 16);
+  if (n < 1 || n > 16) return fail(VT_EINVAL, "%s: bad kernel count %d", path, n);
+  std::lock_guard<std::mutex> lock(g_dyn_mu);
+  int nd = g_ndyn.load(std::memory_order_relaxed);
+  if (nd + n > kMaxDyn) return fail(VT_EINVAL, "too many code modules loaded");
+  for (int i = 0; i < n; ++i) {
+    const vt_module_kernel& m = mk[i];
+    if (m.version != VT_MODULE_VERSION || !m.launch || !m.prepare)
+      return fail(VT_EINVAL, "%s: kernel %d has an incompatible descriptor", path, i);
+    KernelEntry& e = g_dyn[nd + i];
+    e.K = m.K; e.B = m.B; e.T = m.T; e.WPT = m.WPT; e.SL = m.SL; e.CH = m.CH; e.BL = m.BL; e.SQ = m.SQ;
+    e.body = m.body;
+    for (int b = 0; b < VT_MAX_OUTPUTS; ++b) e.gens[b] = m.gens[b];
+    e.fn = nullptr;
+    e.fn_nofm = m.has_nofm ? reinterpret_cast<const void*>(1) : nullptr;  // (a flag: the module picks the function)
+    e.smem = m.smem; e.tc = m.tc; e.nt = m.nt;
+    e.launch = m.launch;
+    e.prepare = m.prepare;
+  }
+  g_ndyn.store(nd + n, std::memory_order_release);
+  return n;
+}
+
 size_t vt_workspace_bytes(const vt_code* code, int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1) {
   const KernelEntry* k = find(code);
   if (!k || N < 1 || F < 1 || V < 0 || w1 <= w0) return 0;
   const Geometry g = geometry(N, F, V, w0, w1, k->CH, k->BL);
-  return scratch_bytes(k, g, launch_grid(k, g, N, F, V, w0, w1));
+  cta_capacity(k);
+  return plan_scratch(k, g, plan_launch(k, g, N, F, V, w0, w1));
 }
 
 int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, int64_t st1, int64_t N, int64_t F,
@@ -250,8 +353,9 @@ int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, 
                 (long long)st1, (long long)need_lo, (long long)need_hi);
 
   const Geometry g = geometry(N, F, V, w0, w1, k->CH, k->BL);
-  const int64_t grid = launch_grid(k, g, N, F, V, w0, w1);
-  const size_t need = scratch_bytes(k, g, grid);
+  cta_capacity(k);  // (prepared once per device)
+  const LaunchPlan p = plan_launch(k, g, N, F, V, w0, w1);
+  const size_t need = plan_scratch(k, g, p);
   if (!workspace || workspace_bytes < need)
     return fail(VT_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
 
@@ -270,12 +374,9 @@ int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, 
   a.nc = g.nc;
   a.b_lo = g.b_lo;
   a.nbs = g.nbs;
-  void* args[] = {&a};
-  const void* fn = (final_metric == nullptr && k->fn_nofm) ? k->fn_nofm : k->fn;
-  cta_capacity(k);  // (prepared once per device)
-  cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(k->nt), args, (size_t)k->smem, (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-  return VT_OK;
+  rc = launch(k, a, w0, p.wh, p.grid_main, stream);
+  if (rc) return rc;
+  return launch(k, a, p.wh, w1, p.grid_tail, stream);
 }
 
 int vt_decode_stream(const vt_code* code, const int8_t* llr, int64_t N, int64_t F, int64_t V, uint32_t* bits,
@@ -321,48 +422,79 @@ int vt_pack_llr_f64(const double* llr, int64_t B, int64_t N, int64_t row_stride,
   return VT_OK;
 }
 
-int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N, int64_t F, int64_t V,
-                          uint32_t* bits_host, int8_t* llr_dev, uint32_t* bits_dev, void* workspace,
-                          size_t workspace_bytes, int nchunks, void* stream) {
-  g_err[0] = 0;
-  int rc = validate(code);
-  if (rc) return rc;
-  if (!find(code)) return fail(VT_EUNSUPPORTED, "no sm_100a kernel compiled for this code");
-  if (N < 1 || F < 1 || V < 0) return fail(VT_EINVAL, "bad geometry");
-  if (!llr_host || !bits_host || !llr_dev || !bits_dev) return fail(VT_EINVAL, "NULL buffer");
-  const int B = code->B;
+}  // extern "C"
+
+namespace {
+
+// Shard g of G: contiguous balanced window range and the stage range (V-stage halos,
+// st0 floored to 16) its windows read (sharding.shard_windows mirrors this).
+void shard_range(int64_t N, int64_t F, int64_t V, int64_t G, int64_t g, int64_t* w0, int64_t* w1, int64_t* st0,
+                 int64_t* st1) {
   const int64_t nw = (N + F - 1) / F;
-  const int64_t nwords = (N + 31) / 32;
+  *w0 = nw * g / G;
+  *w1 = nw * (g + 1) / G;
+  *st0 = (std::max<int64_t>(0, *w0 * F - V) / 16) * 16;
+  *st1 = *w1 > *w0 ? std::min<int64_t>(N, std::min<int64_t>(*w1 * F, N) + V) : *st0;
+}
+
+// Output words of window range [w0, w1): [own_lo, own_hi) hold only its bits; edge[0] /
+// edge[1] (index or -1) are the words it shares with the previous / next range.
+struct WordRange {
+  int64_t own_lo, own_hi, edge[2];
+};
+
+WordRange word_range(int64_t N, int64_t F, int64_t w0, int64_t w1) {
+  WordRange r;
+  const int64_t e0 = w0 * F, e1 = std::min(w1 * F, N), nwords = (N + 31) / 32;
+  r.own_lo = (e0 + 31) / 32;
+  r.own_hi = e1 == N ? nwords : e1 / 32;
+  r.edge[0] = (e0 % 32) ? e0 / 32 : -1;
+  r.edge[1] = (e1 < N && (e1 % 32)) ? e1 / 32 : -1;
+  if (r.edge[0] >= 0 && r.edge[0] == r.edge[1]) r.edge[1] = -1;  // one word shared with both neighbours
+  if (r.own_hi < r.own_lo) r.own_hi = r.own_lo;
+  return r;
+}
+
+// Windows [w0, w1) from host LLRs, pipelined in nchunks window ranges: H2D on one copy
+// stream, the decode on `s`, D2H of the words only this range writes into bits_host on a
+// second copy stream; the shared edge words go to edge_out (merged by the caller).
+// llr_dev holds stages from dst0 (multiple of 16); bits_dev is indexed by stream word.
+int host_range(const vt_code* code, const int8_t* llr_host, int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1,
+               uint32_t* bits_host, int8_t* llr_dev, int64_t dst0, uint32_t* bits_dev, void* workspace,
+               size_t workspace_bytes, int nchunks, cudaStream_t s, uint32_t edge_out[2]) {
+  const int B = code->B;
+  const int64_t nw = w1 - w0;
   if (nchunks < 1) nchunks = 1;
   if (nchunks > nw) nchunks = (int)nw;
-  cudaStream_t s = (cudaStream_t)stream;
-
+  const WordRange wr = word_range(N, F, w0, w1);
   // copy and compute run on separate streams so chunk i+1's H2D overlaps chunk i's decode
-  static thread_local cudaStream_t cs_in = nullptr, cs_out = nullptr;
-  static thread_local int cs_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (cs_dev != dev || !cs_in) {
-    cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking);
-    cs_dev = dev;
+  // (created per call on the current device: the call is a whole-range decode, and
+  // nothing outlives it)
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  if (cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cs_in) cudaStreamDestroy(cs_in);
+    return fail(VT_ECUDA, "cannot create copy streams");
   }
-  cudaError_t e = cudaMemsetAsync(bits_dev, 0, nwords * 4, s);
-  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  const int64_t mlo = (w0 * F) / 32, mhi = (std::min(w1 * F, N) + 31) / 32;
+  int rc = 0;
+  cudaError_t e = cudaMemsetAsync(bits_dev + mlo, 0, (size_t)(mhi - mlo) * 4, s);
+  if (e != cudaSuccess) rc = cuda_fail(e, "memset");
   cudaEvent_t ev_start;
   cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
   cudaEventRecord(ev_start, s);
   cudaStreamWaitEvent(cs_in, ev_start, 0);
   cudaStreamWaitEvent(cs_out, ev_start, 0);
 
-  int64_t copied_hi = 0, words_done = 0;
+  int64_t copied_hi = 0, words_done = wr.own_lo;
   for (int i = 0; i < nchunks && rc == 0; ++i) {
-    const int64_t w0 = nw * i / nchunks, w1 = nw * (i + 1) / nchunks;
-    const int64_t st0 = (std::max<int64_t>(0, w0 * F - V) / 16) * 16;
-    const int64_t st1 = std::min<int64_t>(N, std::min<int64_t>(w1 * F, N) + V);
+    const int64_t c0w = w0 + nw * i / nchunks, c1w = w0 + nw * (i + 1) / nchunks;
+    const int64_t st0 = (std::max<int64_t>(0, c0w * F - V) / 16) * 16;
+    const int64_t st1 = std::min<int64_t>(N, std::min<int64_t>(c1w * F, N) + V);
     const int64_t c0 = std::max(st0, copied_hi);
     if (st1 > c0) {
-      e = cudaMemcpyAsync(llr_dev + c0 * B, llr_host + c0 * B, (size_t)(st1 - c0) * B, cudaMemcpyHostToDevice, cs_in);
+      e = cudaMemcpyAsync(llr_dev + (c0 - dst0) * B, llr_host + c0 * B, (size_t)(st1 - c0) * B, cudaMemcpyHostToDevice,
+                          cs_in);
       if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
       copied_hi = st1;
     }
@@ -371,11 +503,12 @@ int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N
     cudaEventCreateWithFlags(&ev_k, cudaEventDisableTiming);
     cudaEventRecord(ev_in, cs_in);
     cudaStreamWaitEvent(s, ev_in, 0);
-    rc = vt_decode_stream_range(code, llr_dev + st0 * B, st0, st1, N, F, V, w0, w1, bits_dev, nullptr, workspace,
-                                workspace_bytes, s);
+    rc = vt_decode_stream_range(code, llr_dev + (st0 - dst0) * B, st0, st1, N, F, V, c0w, c1w, bits_dev, nullptr,
+                                workspace, workspace_bytes, s);
     cudaEventRecord(ev_k, s);
     cudaStreamWaitEvent(cs_out, ev_k, 0);
-    const int64_t wend = (i + 1 == nchunks) ? nwords : std::min<int64_t>(N, w1 * F) / 32;
+    // words complete after this chunk: all below the next chunk's first emit word
+    const int64_t wend = (i + 1 == nchunks) ? wr.own_hi : std::min<int64_t>(wr.own_hi, std::min(N, c1w * F) / 32);
     if (rc == 0 && wend > words_done) {
       e = cudaMemcpyAsync(bits_host + words_done, bits_dev + words_done, (size_t)(wend - words_done) * 4,
                           cudaMemcpyDeviceToHost, cs_out);
@@ -392,8 +525,116 @@ int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N
   e = cudaStreamSynchronize(s);
   cudaEventDestroy(ev_done);
   cudaEventDestroy(ev_start);
+  cudaStreamDestroy(cs_in);
+  cudaStreamDestroy(cs_out);
   if (rc == 0 && e != cudaSuccess) rc = cuda_fail(e, "decode_stream_host");
+  for (int k = 0; k < 2 && rc == 0; ++k) {
+    edge_out[k] = 0;
+    if (wr.edge[k] >= 0) {
+      e = cudaMemcpy(&edge_out[k], bits_dev + wr.edge[k], 4, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) rc = cuda_fail(e, "edge word");
+    }
+  }
   return rc;
+}
+
+int check_host_args(const vt_code* code, int64_t N, int64_t F, int64_t V, const void* llr_host, const void* bits_host) {
+  int rc = validate(code);
+  if (rc) return rc;
+  if (!find(code)) return fail(VT_EUNSUPPORTED, "no sm_100a kernel compiled for this code");
+  if (N < 1 || F < 1 || V < 0) return fail(VT_EINVAL, "bad geometry");
+  if (!llr_host || !bits_host) return fail(VT_EINVAL, "NULL buffer");
+  return VT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vt_decode_stream_host(const vt_code* code, const int8_t* llr_host, int64_t N, int64_t F, int64_t V,
+                          uint32_t* bits_host, int8_t* llr_dev, uint32_t* bits_dev, void* workspace,
+                          size_t workspace_bytes, int nchunks, void* stream) {
+  g_err[0] = 0;
+  int rc = check_host_args(code, N, F, V, llr_host, bits_host);
+  if (rc) return rc;
+  if (!llr_dev || !bits_dev) return fail(VT_EINVAL, "NULL buffer");
+  uint32_t edge[2];
+  return host_range(code, llr_host, N, F, V, 0, (N + F - 1) / F, bits_host, llr_dev, 0, bits_dev, workspace,
+                    workspace_bytes, nchunks, (cudaStream_t)stream, edge);
+}
+
+int vt_shard_range(int64_t N, int64_t F, int64_t V, int ndev, int g, int64_t out[4]) {
+  g_err[0] = 0;
+  if (N < 1 || F < 1 || V < 0 || ndev < 1 || g < 0 || g >= ndev || !out) return fail(VT_EINVAL, "bad shard request");
+  shard_range(N, F, V, ndev, g, &out[0], &out[1], &out[2], &out[3]);
+  return VT_OK;
+}
+
+size_t vt_workspace_bytes_host(const vt_code* code, int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1,
+                               int nchunks) {
+  const int64_t nw = w1 - w0;
+  if (nw <= 0) return 0;
+  if (nchunks < 1) nchunks = 1;
+  if (nchunks > nw) nchunks = (int)nw;
+  size_t need = 0;
+  for (int i = 0; i < nchunks; ++i) {
+    const int64_t c0 = w0 + nw * i / nchunks, c1 = w0 + nw * (i + 1) / nchunks;
+    if (c1 > c0) need = std::max(need, vt_workspace_bytes(code, N, F, V, c0, c1));
+  }
+  return need;
+}
+
+int vt_decode_stream_host_multi(const vt_code* code, const int8_t* llr_host, int64_t N, int64_t F, int64_t V,
+                                uint32_t* bits_host, int ndev, const int* devices, int8_t* const* llr_dev,
+                                uint32_t* const* bits_dev, void* const* workspace, const size_t* workspace_bytes,
+                                int nchunks) {
+  g_err[0] = 0;
+  int rc = check_host_args(code, N, F, V, llr_host, bits_host);
+  if (rc) return rc;
+  if (ndev < 1 || ndev > 64 || !devices || !llr_dev || !bits_dev || !workspace || !workspace_bytes)
+    return fail(VT_EINVAL, "bad device list");
+  for (int g = 0; g < ndev; ++g)
+    if (!llr_dev[g] || !bits_dev[g]) return fail(VT_EINVAL, "NULL device buffer for shard %d", g);
+  std::vector<int> rcs(ndev, 0);
+  std::vector<std::string> msgs(ndev);
+  std::vector<uint32_t> edges(2 * ndev, 0);
+  std::vector<int64_t> edge_idx(2 * ndev, -1);
+  auto work = [&](int g) {
+    int64_t w0, w1, st0, st1;
+    shard_range(N, F, V, ndev, g, &w0, &w1, &st0, &st1);
+    if (w1 <= w0) return;
+    const WordRange wr = word_range(N, F, w0, w1);
+    edge_idx[2 * g] = wr.edge[0];
+    edge_idx[2 * g + 1] = wr.edge[1];
+    cudaError_t e = cudaSetDevice(devices[g]);
+    if (e != cudaSuccess) { rcs[g] = cuda_fail(e, "cudaSetDevice"); msgs[g] = g_err; return; }
+    cudaStream_t s = nullptr;
+    e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { rcs[g] = cuda_fail(e, "stream"); msgs[g] = g_err; return; }
+    rcs[g] = host_range(code, llr_host, N, F, V, w0, w1, bits_host, llr_dev[g], st0, bits_dev[g], workspace[g],
+                        workspace_bytes[g], nchunks, s, &edges[2 * g]);
+    if (rcs[g]) msgs[g] = g_err;
+    cudaStreamDestroy(s);
+  };
+  std::vector<std::thread> pool;
+  for (int g = 1; g < ndev; ++g) pool.emplace_back(work, g);
+  {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    work(0);
+    cudaSetDevice(cur);
+  }
+  for (auto& t : pool) t.join();
+  for (int g = 0; g < ndev; ++g)
+    if (rcs[g]) return fail(rcs[g], "shard %d (device %d): %s", g, devices[g], msgs[g].c_str());
+  // words shared by two shards: each holds only its own windows' bits, so OR is the merge
+  for (int g = 0; g < ndev; ++g)
+    for (int k = 0; k < 2; ++k)
+      if (edge_idx[2 * g + k] >= 0) bits_host[edge_idx[2 * g + k]] = 0;
+  for (int g = 0; g < ndev; ++g)
+    for (int k = 0; k < 2; ++k)
+      if (edge_idx[2 * g + k] >= 0) bits_host[edge_idx[2 * g + k]] |= edges[2 * g + k];
+  return VT_OK;
 }
 
 }  // extern "C"

@@ -38,6 +38,7 @@ __all__ = [
     "decode_matrix_batch",
     "decode_matrix",
     "workspace_bytes",
+    "release_workspaces",
 ]
 
 _PRECISIONS = ("half", "single")
@@ -148,7 +149,8 @@ def _torch():
 def _workspace(nbytes: int, stream=None):
     """Scratch for one launch, one buffer per (device, stream): launches on one stream are
     ordered, so they may share it; concurrent streams (e.g. worker threads, as
-    framing.decode_stream's workers=) each get their own."""
+    framing.decode_stream's workers=) each get their own.  ``release_workspaces()`` frees
+    them."""
     torch = _torch()
     dev = torch.cuda.current_device()
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -160,6 +162,27 @@ def _workspace(nbytes: int, stream=None):
                 buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=f"cuda:{dev}")
             _ws[key] = buf
         return buf
+
+
+def _pinned(tag: str, numel: int, dtype):
+    """Grow-only pinned host staging buffer per (calling thread, tag): reused across calls
+    (pinning is a page-locking syscall per allocation).  Only for buffers that never
+    leave the call."""
+    torch = _torch()
+    key = ("pinned", tag, threading.get_ident())
+    with _ws_lock:
+        buf = _ws.get(key)
+        if buf is None or buf.numel() < numel or buf.dtype != dtype:
+            buf = torch.empty(max(numel, 1), dtype=dtype, pin_memory=True)
+            _ws[key] = buf
+    return buf[:numel]
+
+
+def release_workspaces() -> None:
+    """Free the cached device workspaces and host staging buffers (they are kept
+    between calls so repeated decodes do not reallocate)."""
+    with _ws_lock:
+        _ws.clear()
 
 
 def _ptr(t) -> ctypes.c_void_p:
@@ -182,9 +205,9 @@ def _code(spec: CodeSpec) -> VtCode:
         return c
     c = VtCode.from_spec(spec)
     if not lib().vt_code_supported(ctypes.byref(c)):
-        raise NotImplementedError(
-            f"no sm_100a kernel was generated for K={spec.constraint_length} generators "
-            f"{spec.octal_generators}; add it to csrc/gen_kernels.py STANDARD_CODES and rebuild")
+        # a code the library was not built with: generate + compile its kernels (jit.py)
+        from . import jit
+        jit.ensure(spec)
     _codes[key] = c
     return c
 
@@ -252,11 +275,35 @@ def decode_stream_device(llr_nb, spec: CodeSpec, frame_len: int, overlap: int, *
     return out
 
 
+def _devices(devices, workers: int) -> list[int]:
+    torch = _torch()
+    if devices is not None:
+        devs = [int(d) for d in devices]
+        if not devs:
+            raise ValueError("devices must not be empty")
+        n = torch.cuda.device_count()
+        for d in devs:
+            if not 0 <= d < n:
+                raise ValueError(f"device {d} out of range (have {n})")
+        return devs
+    workers = int(workers)
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    return list(range(min(workers, torch.cuda.device_count()))) if workers > 1 else [torch.cuda.current_device()]
+
+
 def decode_stream_host(llr_nb_host, spec: CodeSpec, frame_len: int, overlap: int, *, bits_host=None,
-                       nchunks: int = 8, stream=None):
+                       nchunks: int = 8, stream=None, devices=None, workers: int = 1):
     """End-to-end decode through the C-ABI host entry (vt_decode_stream_host):
     int8 (N, B) host tensor (pinned for full PCIe bandwidth) -> packed int32
-    host tensor.  H2D, decode and D2H are pipelined in ``nchunks`` window ranges."""
+    host tensor.  H2D, decode and D2H are pipelined in ``nchunks`` window ranges.
+
+    ``devices`` (CUDA device indices; repeats allowed = several streams on one
+    GPU) or ``workers`` > 1 (the first min(workers, device_count) GPUs) fans the
+    windows out over several devices, one shard, host thread, stream and set of
+    staging buffers each (vt_decode_stream_host_multi) -- the reference's
+    ``workers`` thread fan-out of one stream's windows (framing.py:121-135).
+    Each GPU brings its own PCIe link, so the end-to-end rate scales with them."""
     torch = _torch()
     code = _code(spec)
     n = int(llr_nb_host.shape[0])
@@ -264,8 +311,13 @@ def decode_stream_host(llr_nb_host, spec: CodeSpec, frame_len: int, overlap: int
     nwords = (n + 31) // 32
     if bits_host is None:
         bits_host = torch.empty(nwords, dtype=torch.int32, pin_memory=True)
+    devs = _devices(devices, workers)
+    nw = -(-n // int(frame_len))
+    if len(devs) > 1:
+        return _decode_stream_host_multi(llr_nb_host, code, spec, n, int(frame_len), int(overlap), bits_host,
+                                         devs, int(nchunks))
     dev = torch.cuda.current_device()
-    key = ("host", dev, threading.get_ident())  # the C entry runs on per-thread streams
+    key = ("host", dev, threading.get_ident())  # the C entry runs on per-call copy streams
     with _ws_lock:
         stg = _ws.get(key)
         need_llr = ((n * b + 15) // 16) * 16
@@ -273,16 +325,47 @@ def decode_stream_host(llr_nb_host, spec: CodeSpec, frame_len: int, overlap: int
             stg = (torch.empty(need_llr, dtype=torch.int8, device=f"cuda:{dev}"),
                    torch.empty(nwords, dtype=torch.int32, device=f"cuda:{dev}"))
             _ws[key] = stg
-    nw = -(-n // int(frame_len))
-    need = 0
-    for i in range(max(1, min(nchunks, nw))):
-        w0, w1 = nw * i // nchunks, nw * (i + 1) // nchunks
-        if w1 > w0:
-            need = max(need, lib().vt_workspace_bytes(ctypes.byref(code), n, int(frame_len), int(overlap), w0, w1))
+    need = lib().vt_workspace_bytes_host(ctypes.byref(code), n, int(frame_len), int(overlap), 0, nw, int(nchunks))
     ws = _workspace(need, stream)
     check(lib().vt_decode_stream_host(ctypes.byref(code), _ptr(llr_nb_host), n, int(frame_len), int(overlap),
                                       _ptr(bits_host), _ptr(stg[0]), _ptr(stg[1]), _ptr(ws), ws.numel(),
                                       int(nchunks), _stream_ptr(stream)))
+    return bits_host
+
+
+def _decode_stream_host_multi(llr_nb_host, code, spec, n: int, f: int, v: int, bits_host, devs, nchunks: int):
+    torch = _torch()
+    b = spec.outputs_per_bit
+    nwords = (n + 31) // 32
+    g_n = len(devs)
+    llr_p, bits_p, ws_p, ws_n = [], [], [], []
+    keep = []
+    rng = (ctypes.c_int64 * 4)()
+    for g, d in enumerate(devs):
+        check(lib().vt_shard_range(n, f, v, g_n, g, rng))
+        w0, w1, st0, st1 = (int(x) for x in rng)
+        key = ("multi", d, g, threading.get_ident())
+        with torch.cuda.device(d):
+            need_ws = lib().vt_workspace_bytes_host(ctypes.byref(code), n, f, v, w0, w1, nchunks) if w1 > w0 else 0
+            need_llr = max(16, (((st1 - st0) * b + 15) // 16) * 16)
+            with _ws_lock:
+                stg = _ws.get(key)
+                if (stg is None or stg[0].numel() < need_llr or stg[1].numel() < nwords or
+                        stg[2].numel() < need_ws):
+                    stg = (torch.empty(need_llr, dtype=torch.int8, device=f"cuda:{d}"),
+                           torch.empty(nwords, dtype=torch.int32, device=f"cuda:{d}"),
+                           torch.empty(max(need_ws, 1 << 20), dtype=torch.uint8, device=f"cuda:{d}"))
+                    _ws[key] = stg
+        keep.append(stg)
+        llr_p.append(stg[0].data_ptr())
+        bits_p.append(stg[1].data_ptr())
+        ws_p.append(stg[2].data_ptr())
+        ws_n.append(stg[2].numel())
+    arr = lambda t, xs: (t * len(xs))(*xs)  # noqa: E731
+    check(lib().vt_decode_stream_host_multi(
+        ctypes.byref(code), _ptr(llr_nb_host), n, f, v, _ptr(bits_host), g_n, arr(ctypes.c_int, devs),
+        arr(ctypes.c_void_p, llr_p), arr(ctypes.c_void_p, bits_p), arr(ctypes.c_void_p, ws_p),
+        arr(ctypes.c_size_t, ws_n), nchunks))
     return bits_host
 
 
@@ -317,8 +400,9 @@ def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "referenc
                   config: DecoderConfig | None = None, workers: int = 1) -> np.ndarray:
     """framing.decode_stream (framing.py:96-141): decode a (B, N) LLR stream
     window by window and stitch the emit ranges -> uint8 bits (N,).
-    ``workers`` is accepted for signature compatibility (the GPU decodes all
-    windows of the plan in one launch)."""
+    ``workers`` > 1 fans the windows out over up to that many GPUs (the
+    reference fans them over threads, framing.py:121-135); on one GPU all
+    windows of the plan run in one launch either way."""
     arr = np.asarray(llr)
     if arr.ndim != 2 or arr.shape[1] != plan.total_stages:
         raise ValueError("plan does not match stream length")
@@ -337,9 +421,10 @@ def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "referenc
         # straight into pinned memory, then the pipelined host entry
         a64 = np.ascontiguousarray(arr)
         n = a64.shape[1]
-        pinned = torch.empty((n, a64.shape[0]), dtype=torch.int8, pin_memory=True)
+        pinned = _pinned("llr", n * a64.shape[0], torch.int8).view(n, a64.shape[0])
         check(lib().vt_pack_llr_f64(a64.ctypes.data_as(ctypes.c_void_p), a64.shape[0], n, n, _ptr(pinned), 0))
-        words = decode_stream_host(pinned, spec, plan.frame_len, plan.overlap)
+        words = decode_stream_host(pinned, spec, plan.frame_len, plan.overlap,
+                                   bits_host=_pinned("bits", (n + 31) // 32, torch.int32), workers=workers)
         return _unpack(words.numpy(), n)
     q = _as_int8_llr(arr).T.copy()  # (N, B) stage-major
     n = q.shape[0]
@@ -350,23 +435,40 @@ def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "referenc
         out = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev.device)
         _decode_r4perm_device(dev, spec, n, plan.frame_len, plan.overlap, out)
         return _unpack(out.cpu().numpy(), n)
-    pinned = torch.from_numpy(q).pin_memory()
-    words = decode_stream_host(pinned, spec, plan.frame_len, plan.overlap)
+    pinned = _pinned("llr", q.size, torch.int8).view(n, q.shape[1])
+    pinned.numpy()[...] = q
+    words = decode_stream_host(pinned, spec, plan.frame_len, plan.overlap,
+                               bits_host=_pinned("bits", (n + 31) // 32, torch.int32), workers=workers)
     return _unpack(words.numpy(), n)
 
 
-def _closed_form_plan(plan: FramePlan) -> bool:
+def _closed_form_plan(plan) -> bool:
     """True when the plan's windows are plan_frames(N, F, V)'s (the fused stream kernels
-    compute that geometry on the device)."""
+    compute that geometry on the device).  Any plan object with the reference's
+    FramePlan fields qualifies -- including one built by the reference's own
+    plan_frames (framing.py:68-83, a different Window class): windows are compared by
+    their (start, stop, emit_start, emit_stop) geometry."""
     from .framing import _Windows
     w = plan.windows
+    n, f, v = int(plan.total_stages), int(plan.frame_len), int(plan.overlap)
     if isinstance(w, _Windows):
-        return (w._n, w._f, w._v) == (plan.total_stages, plan.frame_len, plan.overlap)
-    from .framing import plan_frames
-    return tuple(w) == tuple(plan_frames(plan.total_stages, plan.frame_len, plan.overlap).windows)
+        return (w._n, w._f, w._v) == (n, f, v)
+    if n < 1 or f < 1 or v < 0:
+        return False
+    nw = -(-n // f)
+    if len(w) != nw:
+        return False
+    try:
+        got = np.array([(x.start, x.stop, x.emit_start, x.emit_stop) for x in w], dtype=np.int64).reshape(nw, 4)
+    except AttributeError:
+        return False
+    e0 = np.arange(nw, dtype=np.int64) * f
+    e1 = np.minimum(e0 + f, n)
+    want = np.stack([np.maximum(0, e0 - v), np.minimum(n, e1 + v), e0, e1], axis=1)
+    return bool(np.array_equal(got, want))
 
 
-def _decode_windows_general(q: np.ndarray, spec: CodeSpec, plan: FramePlan, decoder: str, config) -> np.ndarray:
+def _decode_windows_general(q: np.ndarray, spec: CodeSpec, plan, decoder: str, config) -> np.ndarray:
     """framing._decode_windows (framing.py:86-93, 112-137) for an arbitrary window list:
     windows grouped by length, each group one batched GPU decode, emit ranges stitched."""
     n = q.shape[0]

@@ -5,8 +5,9 @@ Windows of ``plan_frames(N, F, V)`` are independent (framing.py:96-141:
 stream shards over G ranks with no data exchange: rank g decodes the
 contiguous window range [w0, w1) from the stage range [st0, st1) (its emit
 ranges plus a V-stage halo each side) and writes a disjoint range of packed
-output words.  The only collective is an optional gather of the packed bits
-to one rank.
+output words.  The only collective is an optional all_gather of the packed
+bits (``gather_bits``).  ``shard_windows`` is the Python mirror of the C ABI's
+``vt_shard_range`` (the split ``vt_decode_stream_host_multi`` uses).
 """
 from __future__ import annotations
 
@@ -77,11 +78,46 @@ def decode_stream_sharded(llr_shard_nb, spec, n: int, frame_len: int, overlap: i
     return out
 
 
+def _edges(n: int, frame_len: int, sh: Shard) -> tuple[int, int]:
+    """Words this shard shares with its neighbours (-1: none)."""
+    if sh.num_windows == 0:
+        return -1, -1
+    e0, e1 = sh.w0 * frame_len, min(sh.w1 * frame_len, n)
+    return (e0 // 32 if e0 % 32 else -1), (e1 // 32 if (e1 < n and e1 % 32) else -1)
+
+
 def gather_bits(words, n: int, frame_len: int, overlap: int, group=None):
-    """OR-combine every rank's packed words onto all ranks (boundary words can
-    hold bits of two ranks, so a bitwise OR is the exact merge).  One
-    collective (all_reduce with BOR over int32 words); NCCL on GPUs, gloo on CPU."""
+    """Assemble the whole stream's packed words on every rank from each rank's
+    decode (``decode_stream_sharded``).  One ``all_gather`` of equal-size
+    buffers -- each rank's own word range [word0, word1) padded to the longest,
+    plus the <= 2 words it shares with its neighbours -- so only the words a rank
+    wrote travel (NCCL and gloo both support it; NCCL has no bitwise
+    reductions).  Shared words hold disjoint bits of two ranks and are OR-merged.
+    Returns ``words`` with every word filled."""
+    import torch
     import torch.distributed as dist
 
-    dist.all_reduce(words, op=dist.ReduceOp.BOR, group=group)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    shards = [shard_windows(n, frame_len, overlap, world, r) for r in range(world)]
+    width = max(s.word1 - s.word0 for s in shards) + 2
+    sh = shards[rank]
+    buf = torch.zeros(width, dtype=words.dtype, device=words.device)
+    own = sh.word1 - sh.word0
+    buf[:own] = words[sh.word0:sh.word1]
+    for k, idx in enumerate(_edges(n, frame_len, sh)):
+        if idx >= 0:
+            buf[width - 2 + k] = words[idx]
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    edge_words = []
+    for r, s in enumerate(shards):
+        words[s.word0:s.word1] = parts[r][:s.word1 - s.word0]
+        for k, idx in enumerate(_edges(n, frame_len, s)):
+            if idx >= 0:
+                edge_words.append((idx, parts[r][width - 2 + k]))
+    for idx, _ in edge_words:
+        words[idx] = 0
+    for idx, val in edge_words:
+        words[idx] |= val
     return words

@@ -251,13 +251,16 @@ def test_multi_tile_hard_decision_ties(form):
     np.testing.assert_array_equal(got[s0 + F:], want[F:])
 
 
-@pytest.mark.parametrize("form", [FORMS[0], FORMS[2], FORMS[5], FORMS[1]], ids=["K7", "K9", "K7-tc", "K7r3"])
-def test_multi_tile_padding_skip_does_not_overrun_traceback(form, monkeypatch):
-    """V = 0 (no warm-up groups) with a short last window: the threads of the last,
-    nearly empty tile decode the short window (or a dummy copy of it) and could skip
-    its leading zero padding; the skip is capped so their history stores never
-    overtake the previous tile's traceback fetches (found by tools/stress_forms.py:
-    whole windows garbled)."""
+@pytest.mark.parametrize("form", [FORMS[0], FORMS[2], FORMS[6], FORMS[1], FORMS[3]],
+                         ids=["K7", "K9", "K7-tc", "K7r3", "K8"])
+@pytest.mark.parametrize("tail", [130, 3])
+def test_multi_tile_padding_skip_does_not_overrun_traceback(form, tail, monkeypatch):
+    """V = 0 (no warm-up groups) with a short last window: a 16x2 thread decoding it
+    would skip its leading zero padding, and in a CTA that decodes a tile after
+    another tile its history stores could overtake that tile's traceback fetches
+    (found by tools/stress_forms.py: whole windows garbled).  The host splits such a
+    launch: the persistent grid over the windows before the hazardous suffix, one
+    tile per CTA over the suffix (vt_capi.cu plan_launch)."""
     import torch
 
     import paper_2011_13579_b200 as vt
@@ -266,12 +269,27 @@ def test_multi_tile_padding_skip_does_not_overrun_traceback(form, monkeypatch):
         monkeypatch.setenv("VT_KERNEL_VARIANT", variant)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     F, V = 300, 0
-    nw = 2 * sms * wpc + 16  # the last tile holds 16 windows, the last one 130 stages long
-    n = (nw - 1) * F + 130
-    q = np.random.default_rng(k).integers(-3, 4, size=(n, len(gens))).astype(np.int8)
+    nw = 2 * sms * wpc + 16  # the last tile holds 16 windows, the last one `tail` stages long
+    n = (nw - 1) * F + tail
+    q = np.random.default_rng(k + tail).integers(-3, 4, size=(n, len(gens))).astype(np.int8)
     words = vt.decode_stream_device(torch.from_numpy(q).cuda(), vt.CodeSpec(k, gens), F, V)
     got = np.unpackbits(words.cpu().numpy().view(np.uint8), count=n, bitorder="little")
-    for w in list(range(0, 2 * wpc, 7)) + [nw - 1]:
+    for w in list(range(0, 2 * wpc, 7)) + list(range(nw - 40, nw)):
         s, e = w * F, min(n, (w + 1) * F)
         wb, _ = oracle.decode_batch(np.ascontiguousarray(q[s:e].T[None]), k, gens)
         np.testing.assert_array_equal(got[s:e], wb[0], err_msg=f"window {w}")
+
+
+@pytest.mark.parametrize("form", [FORMS[0], FORMS[2]], ids=["K7", "K9"])
+def test_hazard_split_keeps_workspace_capped(form):
+    """The ragged-tail split costs one extra tile of scratch at most: the workspace of a
+    V = 0 stream with a short last window stays within one CTA tile's slot of the
+    aligned stream's (the earlier whole-launch fallback grew it with the window count)."""
+    import paper_2011_13579_b200 as vt
+    k, gens, wpc, _ = form
+    spec = vt.CodeSpec(k, gens)
+    F = 256
+    for n in (1 << 24, 1 << 26):
+        aligned = vt.workspace_bytes(spec, n, F, 0)
+        ragged = vt.workspace_bytes(spec, n + 5, F, 0)
+        assert ragged <= aligned * 1.01 + 4 * 1024 * 1024, (n, aligned, ragged)

@@ -15,7 +15,7 @@ from paper_2011_13579_b200.sharding import gather_bits, shard_windows
 K, GENS = 7, (0o171, 0o133)
 
 
-def _worker(rank, world, port, n, f, v, q, want, results):
+def _worker(rank, world, port, n, f, v, q, want, results, garbage=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -33,6 +33,11 @@ def _worker(rank, world, port, n, f, v, q, want, results):
         words = torch.from_numpy(np.packbits(bits, bitorder="little").view(np.uint8).copy())
         pad = (-len(words)) % 4
         words = torch.cat([words, torch.zeros(pad, dtype=torch.uint8)]).view(torch.int32).clone()
+        if garbage:  # words this rank did not write must not matter
+            g = torch.randint(-2**31, 2**31 - 1, words.shape, dtype=torch.int32)
+            lo, hi = e0 // 32, -(-e1 // 32)
+            g[lo:hi] = words[lo:hi]
+            words = g
         gather_bits(words, n, f, v)
         got = np.unpackbits(words.numpy().view(np.uint8), count=n, bitorder="little")
         results[rank] = int(np.count_nonzero(got != want))
@@ -64,3 +69,17 @@ def test_gloo_two_ranks_reproduce_whole_stream():
     port = 29500 + (os.getpid() % 2000)
     mp.spawn(_worker, args=(2, port, n, f, v, q, want, results), nprocs=2, join=True)
     assert dict(results) == {0: 0, 1: 0}
+
+
+@pytest.mark.parametrize("world,n,f,v", [(2, 10_001, 100, 20), (3, 3_001, 7, 5), (4, 2_000, 48, 0)])
+def test_gloo_gather_ignores_unwritten_words(world, n, f, v):
+    """all_gather of own ranges + shared edge words (NCCL-compatible): garbage outside a
+    rank's emit range never leaks; tiny frames (F < 32) make several ranks share words."""
+    import oracle
+    _, q = oracle.synthetic_stream(n, K, GENS, ebn0_db=2.0, seed=5)
+    want = oracle.decode_stream(q, K, GENS, f, v, threads=4)
+    mgr = mp.Manager()
+    results = mgr.dict()
+    port = 31500 + (os.getpid() % 2000) + world
+    mp.spawn(_worker, args=(world, port, n, f, v, q, want, results, True), nprocs=world, join=True)
+    assert dict(results) == {r: 0 for r in range(world)}
