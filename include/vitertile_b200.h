@@ -87,12 +87,13 @@ int vt_code_supported(const vt_code* code);
  *     int vtm_kernels(vt_module_kernel* out, int max);
  * and registers it here.  Module kernels launch through the module (its own
  * CUDA runtime registration); everything else is shared with built-in codes. */
-#define VT_MODULE_VERSION 1
-typedef int (*vt_module_launch_fn)(const void* stream_args, long long grid, int no_final_metric, void* stream);
+#define VT_MODULE_VERSION 2
+typedef int (*vt_module_launch_fn)(const void* stream_args, const void* tensor_map, long long grid,
+                                   int no_final_metric, void* stream);
 typedef int (*vt_module_prepare_fn)(int* ctas_per_sm);
 typedef struct vt_module_kernel {
   int32_t version;                 /* VT_MODULE_VERSION */
-  int32_t K, B, T, WPT, SL, CH, BL, SQ, body;
+  int32_t K, B, T, WPT, SL, CH, BL, SQ, body, rows;
   uint32_t gens[VT_MAX_OUTPUTS];
   int32_t smem, tc, nt, has_nofm;
   vt_module_launch_fn launch;      /* returns a cudaError_t value */

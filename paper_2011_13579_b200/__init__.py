@@ -32,6 +32,7 @@ from .decoder import (
     decode_stream_host,
     quantize_llr,
     workspace_bytes,
+    release_workspaces,
 )
 from . import fileio  # noqa: F401  (cli.py file formats)
 from . import sharding  # noqa: F401  (multi-GPU window shards)
@@ -66,6 +67,7 @@ __all__ = [
     "find_dragonfly_groups",
     "quantize_llr",
     "workspace_bytes",
+    "release_workspaces",
 ]
 
 __version__ = "0.1.0"

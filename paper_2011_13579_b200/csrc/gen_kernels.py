@@ -379,7 +379,7 @@ def _gen16_supported(name: str, K: int, gens: tuple[int, ...]) -> bool:
 REGISTRY_HEADER = [
     "// GENERATED by gen_kernels.py -- kernel registry:",
     "// VT_KERNEL(fn, fn without final metrics or nullptr, dynamic smem bytes, tensor-core BM, threads per CTA, K, B, "
-    "lanes/window T, windows/thread, SL, chunk CH, history group BL, uint4/group SQ, body stages, {gens})",
+    "lanes/window T, windows/thread, SL, chunk CH, history group BL, uint4/group SQ, body stages, TMA row lines, {gens})",
     "",
 ]
 
@@ -399,7 +399,7 @@ def code_units(name: str, K: int, gens: tuple[int, ...]) -> list[tuple[str, str,
     units.append((f"vtk_{name}.cu", g.kernel(),
                   [f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);'],
                   [f"VT_KERNEL(vtk_{name}, nullptr, 0, 0, {NT}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, "
-                   f"{g.SQ}, 0, {{{gl}}})"]))
+                   f"{g.SQ}, 0, 0, {{{gl}}})"]))
     lanes = T if K in (8, 9) else 0  # (K=7 over 2 lanes measured 97.6 vs 165 Gbps: DESIGN §9b)
     if lanes:  # packed 16x2 variant over T lanes per window pair
         from gen_kernels16m import Gen16M
@@ -410,7 +410,7 @@ def code_units(name: str, K: int, gens: tuple[int, ...]) -> list[tuple[str, str,
                       [f'extern "C" __global__ void vtk16m_{name}(const vt::StreamArgs a);',
                        f'extern "C" __global__ void vtk16mnf_{name}(const vt::StreamArgs a);'],
                       [f"VT_KERNEL(vtk16m_{name}, &vtk16mnf_{name}, {gm.SMEM}, 0, 128, {K}, {len(gens)}, {lanes}, 2, "
-                       f"{gm.SL}, {gm.CH}, {gm.L}, {gm.SQ}, {gm.P}, {{{gl}}})"]))
+                       f"{gm.SL}, {gm.CH}, {gm.L}, {gm.SQ}, {gm.P}, 0, {{{gl}}})"]))
     if K == 7 and _gen16_supported(name, K, gens):  # packed 16x2 variant: two windows per thread
         import gen_kernels16
         from gen_kernels16 import Gen16
@@ -421,12 +421,14 @@ def code_units(name: str, K: int, gens: tuple[int, ...]) -> list[tuple[str, str,
                           [f'extern "C" __global__ void vtk16tc_{name}(const vt::StreamArgs a);',
                            f'extern "C" __global__ void vtk16tcnf_{name}(const vt::StreamArgs a);'],
                           [f"VT_KERNEL(vtk16tc_{name}, &vtk16tcnf_{name}, {gtc.SMEM}, 1, 128, {K}, {len(gens)}, 1, 2, "
-                           f"{gtc.S}, {gtc.CH}, {gtc.L}, {gtc.S // 16}, {gtc.P}, {{{gl}}})"]))
+                           f"{gtc.S}, {gtc.CH}, {gtc.L}, {gtc.S // 16}, {gtc.P}, 0, {{{gl}}})"]))
+        targ = ", const __grid_constant__ CUtensorMap tmap" if g16.tma else ""
+        rows = g16.RS if g16.tma else 0  # TMA box lines per row (0: no tensor-map parameter)
         units.append((f"vtk16_{name}.cu", g16.kernel(),
-                      [f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a);',
-                       f'extern "C" __global__ void vtk16nf_{name}(const vt::StreamArgs a);'],
+                      [f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a{targ});',
+                       f'extern "C" __global__ void vtk16nf_{name}(const vt::StreamArgs a{targ});'],
                       [f"VT_KERNEL(vtk16_{name}, &vtk16nf_{name}, {g16.SMEM}, 0, {gen_kernels16.NT}, {K}, {len(gens)}, "
-                       f"1, 2, {g16.S}, {g16.CH}, {g16.L}, {g16.S // 16}, {g16.P}, {{{gl}}})"]))
+                       f"1, 2, {g16.S}, {g16.CH}, {g16.L}, {g16.S // 16}, {g16.P}, {rows}, {{{gl}}})"]))
     return units
 
 

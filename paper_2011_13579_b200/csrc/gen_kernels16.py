@@ -94,6 +94,7 @@ class Gen16:
         # 2-bit groups, are left to the s32 kernels: generate() checks `supported`)
         self.supported = self.GPB % 2 == 0
         self.pbr = not tc
+        self.tma = self.pbr and os.environ.get("VT_TMA16", "1") == "1"  # TMA LLR staging (interior warps)
         # 5-body (30-stage) chunks: the traceback settles once per chunk, and 5 bodies x 6 bits
         # + < 32 unwritten bits fit its 64-bit accumulator (6 bodies measured +0.6% but need a
         # mid-chunk settle, -2.5%)
@@ -133,6 +134,9 @@ class Gen16:
         # of 4 (NL = 6: 8-way) or 1 (NL = 8: 32-way)
         self.RS = self.NL | 1 if self.pbr else self.NL
         self.SMEM = (4 * self.RS + ring) * NT * 16  # dynamic shared memory bytes
+        if self.tma:  # the TMA barriers after the rows (keeps the rows' alignment)
+            self.SMEM_TMA_OFF = self.SMEM
+            self.SMEM += 16 * (NT // 32)
         # tensor-core branch metrics (paper formulation): int8 LLR tile x +-8 codeword matrix
         self.tc = tc
         if tc:
@@ -293,6 +297,19 @@ class Gen16:
         self.lines.extend(body)
         return outs
 
+    def tma_issue(self, ind: str, k: str) -> None:
+        """Lane 0: TMA chunk `k` of the warp's A and B window sets into buffer (k & 1):
+        box {16 B, RS lines, 32 rows} from the line of lane 0's window (rows = lanes,
+        2*F*B bytes apart), completion on the warp's mbarrier of that buffer."""
+        e = self.emit
+        box = 16 * self.RS * 32
+        e(f"{ind}{{")
+        e(f"{ind}  const int kb = ({k}) & 1;")
+        e(f"{ind}  vt::mbar_expect_tx(s_bar + 2 * warp + kb, {2 * box}u);")
+        e(f"{ind}  vt::tma_load_rows(llrA(kb), &tmap, (int)((oA + (int64_t)CH * B * ({k})) >> 4), 0, s_bar + 2 * warp + kb);")
+        e(f"{ind}  vt::tma_load_rows(llrB(kb), &tmap, (int)((oB + (int64_t)CH * B * ({k})) >> 4), 0, s_bar + 2 * warp + kb);")
+        e(f"{ind}}}")
+
     TBD = 4  # traceback ring depth (groups prefetched ahead into shared memory)
 
     def tb_fetch(self, ind: str, grp: str, ring: str) -> None:
@@ -427,7 +444,8 @@ class Gen16:
         K, B, S, L, P, CH, NL, NWC = self.K, self.B, self.S, self.L, self.P, self.CH, self.NL, self.NWC
         SQ = S // 16  # uint4 of history words per group per thread
         e = self.emit
-        e(f'extern "C" __global__ void __launch_bounds__({NT}, {MINB16}) {name}(const vt::StreamArgs a) {{')
+        targ = ", const __grid_constant__ CUtensorMap tmap" if self.tma else ""
+        e(f'extern "C" __global__ void __launch_bounds__({NT}, {MINB16}) {name}(const vt::StreamArgs a{targ}) {{')
         nwc = "" if self.pbr else f", NWC = {NWC}"  # (NWC: chunk-wide realignment only)
         e(f"  constexpr int B = {B}, K = {K}, CH = {CH}, NL = {NL}{nwc};")
         e("  const int tid = threadIdx.x;")
@@ -438,6 +456,16 @@ class Gen16:
         e(f"  uint4* const s_tb = smem_dyn + {4 * self.RS * NT};  // (even GPB only)")
         e("  (void)s_tb;")
         e("  const uint64_t pol_last = vt::policy_evict_last();")
+        if self.tma:
+            e(f"  uint64_t* const s_bar = reinterpret_cast<uint64_t*>(smem_dyn + {self.SMEM_TMA_OFF // 16});  // TMA chunk barriers [warp][buffer]")
+            e("  const int warp = tid >> 5, lane = tid & 31;")
+            e("  uint32_t tph = 0;  // phase parity of this warp's two barriers")
+            e("  if (a.tma && lane == 0) {")
+            e("    vt::mbar_init(s_bar + 2 * warp, 1);")
+            e("    vt::mbar_init(s_bar + 2 * warp + 1, 1);")
+            e("    vt::mbar_init_fence();")
+            e("  }")
+            e("  __syncwarp();")
         e("  const int64_t nwin = a.w1 - a.w0;")
         e("  const int64_t buf_bytes = (a.st1 - a.st0) * B;")
         e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {SQ} * {NT} + tid;")
@@ -547,18 +575,37 @@ class Gen16:
         if self.tc:
             e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
         e("    // chunks are staged two ahead (cp.async groups): chunk k lives in buffer k & 1")
+        if self.tma:
+            e("    // TMA staging when every window of the warp is interior (uniform F*B stride) and")
+            e("    // in the buffer: one box per window set and chunk, issued by lane 0")
+            e("    const bool tmaw = a.tma && __all_sync(0xFFFFFFFFu, actA && actB && fastA && fastB);")
+            e("    if (tmaw) {")
+            e("      __syncwarp();  // every lane is done with the previous tile's rows")
+            e("      if (lane == 0) {")
+            e("        vt::fence_proxy_async_smem();")
+            self.tma_issue("        ", "0")
+            e("        if (a.nc > 1) {")
+            self.tma_issue("          ", "1")
+            e("        }")
+            e("      }")
+            e("      vt::mbar_wait_parity(s_bar + 2 * warp, tph & 1u);")
+            e("      tph ^= 1u;")
+            e("    } else {")
+        ind = "      " if self.tma else "    "
         if self.pbr:
-            e(f"    vt::stage_row<NL>(llrA(0), a.llr, buf_bytes, oA, fastA);")
-            e(f"    vt::stage_row<NL>(llrB(0), a.llr, buf_bytes, oB, fastB);")
+            e(f"{ind}vt::stage_row<NL>(llrA(0), a.llr, buf_bytes, oA, fastA);")
+            e(f"{ind}vt::stage_row<NL>(llrB(0), a.llr, buf_bytes, oB, fastB);")
         else:
-            e(f"    vt::stage_row<NL>(llrA(0), a.llr, buf_bytes, oA0, fastA);")
-            e(f"    vt::stage_row<NL>(llrB(0), a.llr, buf_bytes, oB0, fastB);")
-        e("    if (a.nc > 1) {")
-        e(f"      vt::stage_row<NL>(llrA(1), a.llr, buf_bytes, oA + (int64_t)CH * B, fastA);")
-        e(f"      vt::stage_row<NL>(llrB(1), a.llr, buf_bytes, oB + (int64_t)CH * B, fastB);")
-        e("    }")
-        e("    vt::cp_async_commit();")
-        e("    vt::cp_async_wait_group<0>();")
+            e(f"{ind}vt::stage_row<NL>(llrA(0), a.llr, buf_bytes, oA0, fastA);")
+            e(f"{ind}vt::stage_row<NL>(llrB(0), a.llr, buf_bytes, oB0, fastB);")
+        e(f"{ind}if (a.nc > 1) {{")
+        e(f"{ind}  vt::stage_row<NL>(llrA(1), a.llr, buf_bytes, oA + (int64_t)CH * B, fastA);")
+        e(f"{ind}  vt::stage_row<NL>(llrB(1), a.llr, buf_bytes, oB + (int64_t)CH * B, fastB);")
+        e(f"{ind}}}")
+        e(f"{ind}vt::cp_async_commit();")
+        e(f"{ind}vt::cp_async_wait_group<0>();")
+        if self.tma:
+            e("    }")
         zb0A = f"(int)min(max((gA.s - gA.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B)"
         zb0B = f"(int)min(max((gB.s - gB.g0 - (int64_t)it0 * {P}) * B, (int64_t)0), (int64_t)CH * B)"
         if self.tc:
@@ -637,13 +684,30 @@ class Gen16:
             e("        tc_issue(c & 1, 1);")
             e("      }")
         else:
-            e("      // chunk c's rows are consumed: stage chunk c+2 into its buffer (rides on the next")
-            e("      // traceback step's commit group, >= 4 steps before chunk c+2 starts)")
-            e("      if (c + 2 < a.nc) {")
-            e(f"        vt::stage_row_rel<NL>(llrA(c & 1), a.llr, buf_bytes, oA, CH * B * (c + 2), fastA);")
-            e(f"        vt::stage_row_rel<NL>(llrB(c & 1), a.llr, buf_bytes, oB, CH * B * (c + 2), fastB);")
-            e("      }")
-            e(f"      if (c + 1 < a.nc) vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 landed")
+            if self.tma:
+                e("      if (tmaw) {  // chunk c's rows are consumed: TMA chunk c+2 into its buffer")
+                e("        if (c + 2 < a.nc) {")
+                e("          __syncwarp();")
+                e("          if (lane == 0) {")
+                e("            vt::fence_proxy_async_smem();")
+                self.tma_issue("            ", "c + 2")
+                e("          }")
+                e("        }")
+                e("        if (c + 1 < a.nc) {  // chunk c+1 landed")
+                e("          vt::mbar_wait_parity(s_bar + 2 * warp + ((c + 1) & 1), (tph >> ((c + 1) & 1)) & 1u);")
+                e("          tph ^= 1u << ((c + 1) & 1);")
+                e("        }")
+                e("      } else {")
+            ind = "        " if self.tma else "      "
+            e(f"{ind}// chunk c's rows are consumed: stage chunk c+2 into its buffer (rides on the next")
+            e(f"{ind}// traceback step's commit group, >= 4 steps before chunk c+2 starts)")
+            e(f"{ind}if (c + 2 < a.nc) {{")
+            e(f"{ind}  vt::stage_row_rel<NL>(llrA(c & 1), a.llr, buf_bytes, oA, CH * B * (c + 2), fastA);")
+            e(f"{ind}  vt::stage_row_rel<NL>(llrB(c & 1), a.llr, buf_bytes, oB, CH * B * (c + 2), fastB);")
+            e(f"{ind}}}")
+            e(f"{ind}if (c + 1 < a.nc) vt::cp_async_wait_group<{self.TBD - 1}>();  // chunk c+1 landed")
+            if self.tma:
+                e("      }")
         e("    }")
         e("    // the previous tile's remaining traceback steps, then its unstored tail")
         e("    while (tbb >= a.b_lo) {")

@@ -62,6 +62,7 @@ Geometry geometry(int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1, int C
 struct KernelEntry {
   int K, B, T, WPT, SL, CH, BL, SQ;
   int body;  // stages per loop body of the 16x2 forms (the unit of the leading-padding skip); 0 for s32
+  int rows;  // > 0: the kernel takes a TMA tensor map of its LLR chunk rows (16-byte lines per row)
   uint32_t gens[VT_MAX_OUTPUTS];
   const void* fn;
   const void* fn_nofm;  // variant without final-metric bookkeeping (nullptr: use fn)
@@ -74,8 +75,8 @@ struct KernelEntry {
   vt_module_prepare_fn prepare;
 };
 
-#define VT_KERNEL(fn_, fnnf_, smem_, tc_, nt_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, BODY_, ...) \
-  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, BODY_, __VA_ARGS__, (const void*)&fn_, (const void*)(fnnf_), smem_, tc_, nt_, \
+#define VT_KERNEL(fn_, fnnf_, smem_, tc_, nt_, K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, BODY_, ROWS_, ...) \
+  {K_, B_, T_, WPT_, SL_, CH_, BL_, SQ_, BODY_, ROWS_, __VA_ARGS__, (const void*)&fn_, (const void*)(fnnf_), smem_, tc_, nt_, \
    nullptr, nullptr},
 }  // namespace
 #include "gen/registry_decl.inc"
@@ -260,18 +261,56 @@ size_t plan_scratch(const KernelEntry* k, const Geometry& g, const LaunchPlan& p
   return scratch_bytes(k, g, std::max(p.grid_main, p.grid_tail));
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda
+// dependency: the library also loads on machines without a driver, e.g. to size workspaces)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// The 16x2 kernels' TMA view of the launch's LLR buffer: lines of 16 bytes, and rows (a warp's
+// same-parity windows) 2*F*B bytes apart; box = one chunk row of `rows` lines for 32 windows.
+// Returns false (the kernels then stage per thread) when the geometry does not allow it.
+bool encode_rows_map(const KernelEntry* k, const vt::StreamArgs& a, CUtensorMap* map) {
+  if (k->rows <= 0 || getenv("VT_NO_TMA")) return false;
+  const int64_t stride = 2 * a.F * k->B, buf_bytes = (a.st1 - a.st0) * k->B;
+  if (stride % 16 != 0 || stride >= ((int64_t)1 << 40) || buf_bytes < 16) return false;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {16, (cuuint64_t)(buf_bytes / 16), 32};
+  const cuuint64_t strides[2] = {16, (cuuint64_t)stride};
+  const cuuint32_t box[3] = {16, (cuuint32_t)k->rows, 32}, es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(a.llr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int launch(const KernelEntry* k, vt::StreamArgs a, int64_t w0, int64_t w1, int64_t grid, void* stream) {
   if (w1 <= w0 || grid <= 0) return VT_OK;
   if (a.final_metric) a.final_metric += (w0 - a.w0);
   a.w0 = w0;
   a.w1 = w1;
+  alignas(64) CUtensorMap map;
+  memset(&map, 0, sizeof(map));
+  a.tma = encode_rows_map(k, a, &map) ? 1 : 0;
   const bool nofm = a.final_metric == nullptr && k->fn_nofm;
   if (k->launch) {
-    const int e = k->launch(&a, (long long)grid, nofm ? 1 : 0, stream);
+    const int e = k->launch(&a, &map, (long long)grid, nofm ? 1 : 0, stream);
     if (e != 0) return cuda_fail((cudaError_t)e, "kernel launch (code module)");
     return VT_OK;
   }
-  void* args[] = {&a};
+  void* args[] = {&a, &map};
   const void* fn = nofm ? k->fn_nofm : k->fn;
   cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(k->nt), args, (size_t)k->smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
@@ -308,6 +347,7 @@ int vt_load_code_module(const char* path) {
     KernelEntry& e = g_dyn[nd + i];
     e.K = m.K; e.B = m.B; e.T = m.T; e.WPT = m.WPT; e.SL = m.SL; e.CH = m.CH; e.BL = m.BL; e.SQ = m.SQ;
     e.body = m.body;
+    e.rows = m.rows;
     for (int b = 0; b < VT_MAX_OUTPUTS; ++b) e.gens[b] = m.gens[b];
     e.fn = nullptr;
     e.fn_nofm = m.has_nofm ? reinterpret_cast<const void*>(1) : nullptr;  // (a flag: the module picks the function)
@@ -374,6 +414,7 @@ int vt_decode_stream_range(const vt_code* code, const int8_t* llr, int64_t st0, 
   a.nc = g.nc;
   a.b_lo = g.b_lo;
   a.nbs = g.nbs;
+  a.tma = 0;
   rc = launch(k, a, w0, p.wh, p.grid_main, stream);
   if (rc) return rc;
   return launch(k, a, p.wh, w1, p.grid_tail, stream);

@@ -8,6 +8,7 @@
 // addressing and the traceback / packed-bit emission.
 #pragma once
 #include <cstdint>
+#include <cuda.h>  // (CUtensorMap only: the map is encoded on the host, vt_capi.cu)
 #include <cuda_runtime.h>
 
 namespace vt {
@@ -24,6 +25,10 @@ struct StreamArgs {
   int nc;                 // BL-stage chunks per window (uniform for the launch; BL = kernel block length)
   int b_lo;               // first chunk whose histories are stored
   int nbs;                // stored chunks per window (nc - b_lo)
+  int tma;                // 1: the kernel's tensor-map parameter is valid (16x2 kernels stage LLR
+                          // chunk rows with TMA): 3-D map over llr {16 bytes, 16-byte lines, 32 rows
+                          // 2*F*B bytes apart} -- one box is the chunk rows of a warp's 32
+                          // same-parity windows (interior windows are F*B bytes apart)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -107,6 +112,32 @@ __device__ __forceinline__ void st_global_v4_hint(uint4* p, uint4 v, uint64_t po
   asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y),
                "r"(v.z), "r"(v.w), "l"(pol)
                : "memory");
+}
+
+// --- TMA (cp.async.bulk.tensor) + mbarrier completion (the 16x2 kernels' LLR staging) ---
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
+                 : "=r"(done) : "r"(b), "r"(parity) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// box {16, lines, rows} at coordinates (0, line, row) -> dst (rows of lines*16 bytes), completes on bar
+__device__ __forceinline__ void tma_load_rows(void* dst, const CUtensorMap* map, int line, int row, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(map), "r"(0), "r"(line), "r"(row),
+      "r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
 }
 
 // Window geometry of window w (framing.py:78-82) in the end-aligned chunk frame.

@@ -12,8 +12,9 @@ tests/golden/golden_r2.npz:
   optimisation is not effective (codes.py:351-412).
 * ``ber``: run_point's own sample recipe (generate_bits / encode_batch /
   modulate_awgn, channel.py:113-136) quantised to int8 (q = clamp(rint(16 y)))
-  and decoded by the reference's decode_batch: error counts per Eb/N0 point,
-  plus the reference's float-LLR run_point count on the same samples.
+  and decoded by the reference's decode_batch: error counts per Eb/N0 point (and
+  per frame: errors come in bursts, so confidence intervals use the frame-level
+  variance), plus the reference's float-LLR run_point count on the same samples.
 """
 from __future__ import annotations
 
@@ -119,10 +120,11 @@ def main():
         y = modulate_awgn(encode_batch(bits, spec), ch, 0.5, idx)  # (F, N, B)
         q = np.clip(np.rint(16.0 * y), -127, 127)
         dec, _ = decode_batch(np.transpose(q, (0, 2, 1)), spec)
-        errors_q = int(np.count_nonzero(dec != bits))
+        frame_errors = np.count_nonzero(dec != bits, axis=1).astype(np.int32)
+        errors_q = int(frame_errors.sum())
         ref_float = run_point(spec, ebn0, BER_BITS, seed=BER_SEED, frame_len=flen, point_index=idx)
         add("ber", code="k7r2", ebn0_db=ebn0, point_index=idx, seed=BER_SEED, frame_len=flen, n=int(bits.size),
-            errors_int8=errors_q, errors_float=int(ref_float.errors))
+            errors_int8=errors_q, errors_float=int(ref_float.errors), frame_errors=frame_errors)
         print(f"BER point {ebn0} dB: int8 {errors_q} errors, float {ref_float.errors} / {bits.size}")
 
     data["index_json"] = np.frombuffer(json.dumps(index).encode(), dtype=np.uint8)

@@ -214,16 +214,19 @@ def test_ber_point_paired_with_reference_samples(vt, case):
 
 
 @pytest.mark.parametrize("case", R2_BER, ids=[f"{c['ebn0_db']}dB" for c in R2_BER])
-def test_ber_point_gpu_rng_within_confidence_of_reference(vt, case):
+def test_ber_point_gpu_rng_within_confidence_of_reference(vt, z2, case):
     """The fused GPU channel (independent Philox samples, 2^27 bits per point) agrees
     with the reference's int8 and float-LLR run_point counts within Monte-Carlo
-    confidence: |z| < 4 with the binomial variance widened 5x for error bursts."""
+    confidence: |z| < 4, with the variance of a point's BER taken from the reference's
+    per-frame error counts (frames are independent; errors within a frame come in
+    bursts: 3x to 18x the binomial variance from 4 dB down to 1 dB)."""
     from paper_2011_13579_b200 import channel as ch
-    g = ch.run_point(vt.default_spec(), case["ebn0_db"], 1 << 27, seed=123, frame_len=case["frame_len"],
+    flen = case["frame_len"]
+    g = ch.run_point(vt.default_spec(), case["ebn0_db"], 1 << 27, seed=123, frame_len=flen,
                      point_index=case["point_index"], rng="gpu")
+    fe = z2[case["key"] + "_frame_errors"].astype(np.float64)
+    var_frame = fe.var(ddof=1) / flen ** 2  # variance of one frame's BER
+    n_ref_frames, n_gpu_frames = case["n"] // flen, g.n // flen
+    s = math.sqrt(var_frame / n_ref_frames + var_frame / n_gpu_frames)
     for ref_err in (case["errors_int8"], case["errors_float"]):
-        p_ref = ref_err / case["n"]
-        p = g.errors / g.n
-        pooled = (ref_err + g.errors) / (case["n"] + g.n)
-        s = math.sqrt(5 * pooled * (1 - pooled) * (1 / case["n"] + 1 / g.n))
-        assert abs(p - p_ref) < 4 * s + 1e-12, (case, g)
+        assert abs(g.errors / g.n - ref_err / case["n"]) < 4 * s + 1e-12, (case["ebn0_db"], ref_err, g)
