@@ -201,6 +201,42 @@ int vt_decode_stream_r4perm(const vt_code* code, const uint8_t* prio, const int8
                             int64_t N, int64_t F, int64_t V, int64_t w0, int64_t w1, uint32_t* bits,
                             int64_t* final_metric, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- the paper's tile formulation on tensor cores ----
+ * matrix.decode_matrix_batch (matrix.py:277-409; tile.py:61-89): every tile op
+ * D = A x B + C runs as two mma.sync.m16n8k16 (f16 x f16 -> f32).  A program is
+ * the reference's pack_radix2 / pack_radix4 tile set (matrix.py:129-265) in
+ * per-lane fragment form (built by paper_2011_13579_b200/tiles.py); every
+ * table pointer is DEVICE memory, the struct itself is passed by host pointer.
+ *   a_frag    [ntiles][32 lanes][4]  A fragment registers (f16x2)
+ *   b_sel     [ntiles][32][8]        LLR index of each B fragment element (-1: 0)
+ *   c_state   [ntiles][32][8]        path metric of each C fragment element (-1: 0)
+ *   cand      [ntiles][nout][4]      candidate D elements (row * 16 + col)
+ *   out_state [ntiles][nout]         state each output updates (-1: none)
+ *   code      [ntiles][nout][4]      survivor value of each candidate */
+typedef struct vt_tile_program {
+  int32_t ntiles, nout, ncand, nllr;
+  const uint32_t* a_frag;
+  const int8_t* b_sel;
+  const int16_t* c_state;
+  const uint8_t* cand;
+  const int16_t* out_state;
+  const uint8_t* code;
+} vt_tile_program;
+
+/* F frames of N stages, llr device (F, N, B) int8.  radix 2: every step on r2;
+ * radix 4: two-stage steps on r4 and a final r2 step for odd N (matrix.py:367-376).
+ * half_acc != 0 rounds every tile result to binary16 (accumulator="half");
+ * renormalize subtracts each step's maximum (offset, float64, per frame).
+ * Device outputs: bits (F, N) uint8 (matrix._traceback_steps), final_metric
+ * (F) float64 (max metric + renormalisation offset, matrix.py:384) and
+ * *mma_count += the mma.sync instructions issued (2 per 16x16x16 tile op);
+ * device scratch: survivors (F, steps, S) uint8, final_lambda (F, S) float32,
+ * offset (F) float64 (steps = N for radix 2, ceil(N/2) for radix 4). */
+int vt_matrix_forward(const vt_code* code, const int8_t* llr, int64_t F, int64_t N, const vt_tile_program* r2,
+                      const vt_tile_program* r4, int radix, int half_acc, int renormalize, uint8_t* survivors,
+                      float* final_lambda, double* offset, uint8_t* bits, double* final_metric,
+                      unsigned long long* mma_count, void* stream);
+
 /* ---- BER harness (channel.py:69-99 of the reference) ---- */
 
 /* Synthetic AWGN/BPSK frames on the device: `frames` frames of frame_len

@@ -66,6 +66,9 @@ def lib():
     L.vt_shard_range.argtypes = [i64, i64, i64, ctypes.c_int, ctypes.c_int, p(i64)]
     L.vt_decode_stream_host_multi.argtypes = [code_p, vp, i64, i64, i64, vp, ctypes.c_int, p(ctypes.c_int), p(vp),
                                               p(vp), p(vp), p(ctypes.c_size_t), ctypes.c_int]
+    L.vt_matrix_forward.argtypes = [code_p, vp, i64, i64, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp,
+                                    vp, vp, vp, vp]
+    L.vt_matrix_forward.restype = ctypes.c_int
     L.vt_channel_awgn.argtypes = [code_p, ctypes.c_uint64, ctypes.c_uint32, i64, i64, ctypes.c_float, ctypes.c_float,
                                   ctypes.c_int, vp, vp, vp]
     L.vt_count_bit_errors.argtypes = [vp, vp, i64, vp, vp]

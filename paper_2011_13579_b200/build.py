@@ -44,7 +44,8 @@ def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     gen_files = gen_kernels.generate(os.path.join(CSRC, "gen"))
     srcs = gen_files + [os.path.join(CSRC, "vt_capi.cu"), os.path.join(CSRC, "vt_channel.cu"),
-                        os.path.join(CSRC, "vt_matrix_r4.cu"), os.path.join(CSRC, "vt_forward.cu")]
+                        os.path.join(CSRC, "vt_matrix_r4.cu"), os.path.join(CSRC, "vt_forward.cu"),
+                        os.path.join(CSRC, "vt_tiles.cu")]
     with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
         results = list(ex.map(_compile, srcs))
     if verbose:

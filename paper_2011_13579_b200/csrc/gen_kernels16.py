@@ -139,6 +139,8 @@ class Gen16:
             self.SMEM += 16 * (NT // 32)
         # tensor-core branch metrics (paper formulation): int8 LLR tile x +-8 codeword matrix
         self.tc = tc
+        # tc: rows-ready mbarrier instead of a CTA-wide __syncthreads before each MMA issue
+        self.tc_mbar = tc and os.environ.get("VT_TC_SYNC", "mbar") == "mbar"
         if tc:
             assert self.cheap and self.B == 2 and self.CH * self.B <= 24 and NT == 128
             self.TCN = self.CH * 4           # MMA N: 4 pattern sums per stage of a chunk
@@ -488,6 +490,8 @@ class Gen16:
             e(f"  char* const s_tc = reinterpret_cast<char*>(smem_dyn) + {self.TCOFF};")
             e("  uint64_t* const tc_bar = reinterpret_cast<uint64_t*>(s_tc + 4 * 4096 + 2048);")
             e("  uint32_t* const tc_tm = reinterpret_cast<uint32_t*>(s_tc + 4 * 4096 + 2048 + 16);")
+            if self.tc_mbar:
+                e("  uint64_t* const rows_bar = reinterpret_cast<uint64_t*>(s_tc + 4 * 4096 + 2048 + 32);  // rows ready")
             e(f"  for (int i = tid; i < {TCN} * 32; i += {NT}) {{")
             e("    const int n = i >> 5, k = i & 31, st = n >> 2, pp = n & 3;")
             e("    int v = 0;")
@@ -501,6 +505,9 @@ class Gen16:
             e("  if (tid == 0) {")
             e("    vt::tc::mbar_init(tc_bar, 1);")
             e("    vt::tc::mbar_init(tc_bar + 1, 1);")
+            if self.tc_mbar:
+                e(f"    vt::tc::mbar_init(rows_bar, {NT});")
+                e(f"    vt::tc::mbar_init(rows_bar + 1, {NT});")
             e('    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");')
             e("  }")
             e("  vt::tc::fence_proxy_async();")
@@ -521,21 +528,43 @@ class Gen16:
             e("    *reinterpret_cast<uint4*>(tb + vt::tc::kmaj(tid, 0)) = make_uint4(wb[0], wb[1], wb[2], wb[3]);")
             e("    *reinterpret_cast<uint2*>(tb + vt::tc::kmaj(tid, 16)) = make_uint2(wb[4], wb[5]);")
             e("  };")
-            e("  // all rows written -> one thread issues the two MMAs of chunk buffer buf")
-            e("  auto tc_issue = [&](int buf0, int nbuf) {")
-            e("    vt::tc::fence_before();")
-            e("    vt::tc::fence_proxy_async();")
-            e("    __syncthreads();")
-            e("    if (tid == 0) {")
-            e("      vt::tc::fence_after();")
-            e("      for (int bb = buf0; bb < buf0 + nbuf; ++bb) {")
-            e("        const uint32_t ab = vt::tc::smem_u32(s_tc + (2 * bb) * 4096);")
-            e(f"        vt::tc::mma_i8(tmb + bb * 128, vt::tc::desc_kmaj(ab), tc_db, TC_ID);")
-            e(f"        vt::tc::mma_i8(tmb + bb * 128 + {TCN}, vt::tc::desc_kmaj(ab + 4096), tc_db, TC_ID);")
-            e("        vt::tc::commit(tc_bar + bb);")
-            e("      }")
-            e("    }")
-            e("  };")
+            if self.tc_mbar:
+                e("  // all rows written -> one thread issues the two MMAs of chunk buffer buf.  No CTA-wide")
+                e("  // barrier: every thread arrives on the buffer's rows-ready mbarrier (count NT) and moves")
+                e("  // on; only the issuing thread waits for the arrivals")
+                e("  uint32_t rows_phase = 0;")
+                e("  auto tc_issue = [&](int buf0, int nbuf) {")
+                e("    vt::tc::fence_before();")
+                e("    vt::tc::fence_proxy_async();")
+                e("    for (int bb = buf0; bb < buf0 + nbuf; ++bb) vt::tc::mbar_arrive(rows_bar + bb);")
+                e("    if (tid == 0) {")
+                e("      for (int bb = buf0; bb < buf0 + nbuf; ++bb) {")
+                e("        vt::tc::mbar_wait(rows_bar + bb, (rows_phase >> bb) & 1u);")
+                e("        rows_phase ^= 1u << bb;")
+                e("        vt::tc::fence_after();")
+                e("        const uint32_t ab = vt::tc::smem_u32(s_tc + (2 * bb) * 4096);")
+                e(f"        vt::tc::mma_i8(tmb + bb * 128, vt::tc::desc_kmaj(ab), tc_db, TC_ID);")
+                e(f"        vt::tc::mma_i8(tmb + bb * 128 + {TCN}, vt::tc::desc_kmaj(ab + 4096), tc_db, TC_ID);")
+                e("        vt::tc::commit(tc_bar + bb);")
+                e("      }")
+                e("    }")
+                e("  };")
+            else:
+                e("  // all rows written -> one thread issues the two MMAs of chunk buffer buf")
+                e("  auto tc_issue = [&](int buf0, int nbuf) {")
+                e("    vt::tc::fence_before();")
+                e("    vt::tc::fence_proxy_async();")
+                e("    __syncthreads();")
+                e("    if (tid == 0) {")
+                e("      vt::tc::fence_after();")
+                e("      for (int bb = buf0; bb < buf0 + nbuf; ++bb) {")
+                e("        const uint32_t ab = vt::tc::smem_u32(s_tc + (2 * bb) * 4096);")
+                e(f"        vt::tc::mma_i8(tmb + bb * 128, vt::tc::desc_kmaj(ab), tc_db, TC_ID);")
+                e(f"        vt::tc::mma_i8(tmb + bb * 128 + {TCN}, vt::tc::desc_kmaj(ab + 4096), tc_db, TC_ID);")
+                e("        vt::tc::commit(tc_bar + bb);")
+                e("      }")
+                e("    }")
+                e("  };")
         e("  // history words of group grp: 4 states per 32-bit word (L bits each, +16 for window B);")
         e("  // traced tile: group grp sits at slot position x = txa + txs * grp (tiles alternate the order)")
         e("  int txa = -a.b_lo, txs = 1;  // (initial values keep the idle prefetches inside the slot)")

@@ -16,6 +16,7 @@
 
 #include "../../include/vitertile_b200.h"
 #include "vt_common.cuh"
+#include "vt_internal.h"
 
 namespace {
 
@@ -28,6 +29,15 @@ int fail(int code, const char* fmt, ...) {
   va_end(ap);
   return code;
 }
+
+}  // namespace
+
+int vt_set_error(int code, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+
+namespace {
 
 int cuda_fail(cudaError_t e, const char* what) {
   return fail(VT_ECUDA, "%s: %s", what, cudaGetErrorString(e));

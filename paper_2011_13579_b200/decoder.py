@@ -46,9 +46,10 @@ _PRECISIONS = ("half", "single")
 
 @dataclass(frozen=True)
 class PrecisionPolicy:
-    """Accumulator / channel-input precision (tile.py:21-31).  The B200 path
-    accumulates exact int32 metrics; ``accumulator="half"`` (a lossy fp16
-    emulation) is rejected at decode time."""
+    """Accumulator / channel-input precision (tile.py:21-31).  The fused decoders
+    accumulate exact integer metrics; the tile decoder (decode_matrix_batch,
+    decoder="matrix") reproduces ``accumulator="half"``: every tensor-core tile
+    result is rounded to binary16 as the reference does."""
 
     accumulator: str = "single"
     channel_input: str = "single"
@@ -410,13 +411,15 @@ def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "referenc
         raise ValueError(f"unknown decoder {decoder!r}")
     if arr.shape[0] != spec.outputs_per_bit:
         raise ValueError("LLR input must have shape (B, N)")
-    r4perm = False
+    r4perm = half = False
     if decoder == "matrix":
         cfg = config or DecoderConfig()
         _, _, effective = _check_matrix_config(spec, cfg)
         r4perm = cfg.radix == 4 and cfg.optimized and effective
+        # the binary16 accumulator rounds metrics (tile.py:87-89): the tile decoder, per window
+        half = cfg.policy.accumulator == "half"
     torch = _torch()
-    if arr.dtype == np.float64 and not r4perm and _closed_form_plan(plan):
+    if arr.dtype == np.float64 and not r4perm and not half and _closed_form_plan(plan):
         # reference-style float LLRs: one native pass checks, converts and transposes
         # straight into pinned memory, then the pipelined host entry
         a64 = np.ascontiguousarray(arr)
@@ -428,7 +431,7 @@ def decode_stream(llr, spec: CodeSpec, plan: FramePlan, decoder: str = "referenc
         return _unpack(words.numpy(), n)
     q = _as_int8_llr(arr).T.copy()  # (N, B) stage-major
     n = q.shape[0]
-    if not _closed_form_plan(plan):
+    if half or not _closed_form_plan(plan):
         return _decode_windows_general(q, spec, plan, decoder, config)
     if r4perm:  # radix-4 with the dragonfly permutation tie order (matrix.py:329-333)
         dev = torch.from_numpy(q).cuda()
@@ -571,9 +574,6 @@ def _radix4_tiles(spec: CodeSpec, optimized: bool) -> tuple[int, bool]:
 
 
 def _check_matrix_config(spec: CodeSpec, config: DecoderConfig) -> tuple[int, int, bool]:
-    if config.policy.accumulator == "half":
-        raise NotImplementedError("accumulator='half' is a lossy fp16 emulation; the B200 decoder accumulates "
-                                  "exact integer metrics and does not reproduce it")
     t2 = _radix2_tiles(spec)
     t4, effective = (_radix4_tiles(spec, config.optimized) if config.radix == 4 else (0, False))
     return t2, t4, effective
@@ -606,41 +606,53 @@ def _decode_r4perm_device(llr_nb, spec: CodeSpec, n: int, frame_len: int, overla
 
 
 def decode_matrix_batch(llrs, spec: CodeSpec, config: DecoderConfig | None = None) -> MatrixDecodeResult:
-    """matrix.decode_matrix_batch (matrix.py:342-386) on the B200 kernels.
-
-    Radix-2 and radix-4 (non-optimised) decisions equal two-stage radix-2 ACS
-    with the natural tie rule, so the fast kernel
-    serves both; radix-4 with an effective dragonfly-group optimisation breaks
-    ties in the representative's permuted order and runs on the r4perm kernel.
-    The counter reports the paper's tile-op accounting."""
+    """matrix.decode_matrix_batch (matrix.py:342-386) in the paper's formulation on
+    tensor cores: every tile op D = A x B + C of the reference's pack_radix2 /
+    pack_radix4 tiles (radix 2, radix 4, radix 4 with the dragonfly-permutation
+    groups) runs as mma.sync.m16n8k16 (vt_matrix_forward, csrc/vt_tiles.cu); the
+    counter reports the tile ops the kernel actually issued.  ``accumulator="half"``
+    rounds every tile result to binary16 exactly as tile.py:87-89 does."""
     config = config or DecoderConfig()
     arr = np.asarray(llrs, dtype=np.float32)
     if arr.ndim != 3 or arr.shape[1] != spec.outputs_per_bit:
         raise ValueError("LLR batch must have shape (F, B, N)")
-    f, _, n = arr.shape
-    t2, t4, effective = _check_matrix_config(spec, config)
+    f, b, n = arr.shape
+    _check_matrix_config(spec, config)
     # matrix.py:290,320 (and 354-355): LLRs pass through binary16; exact for int8 values
-    arr = arr.astype(np.float16).astype(np.float64)
-    q = _as_int8_llr(arr)
-    if config.radix == 4 and config.optimized and effective:
-        torch = _torch()
-        dev = torch.from_numpy(np.ascontiguousarray(np.transpose(q, (0, 2, 1)))).cuda().reshape(f * n, -1)
-        out = torch.zeros((f * n + 31) // 32, dtype=torch.int32, device=dev.device)
-        fm = torch.empty(f, dtype=torch.int64, device=dev.device)
-        _decode_r4perm_device(dev, spec, f * n, n, 0, out, fm)
-        bits = _unpack(out.cpu().numpy(), f * n).reshape(f, n)
-        metric = fm.cpu().numpy()
-    else:
-        bits, metric = _decode_frames_np(np.transpose(q, (0, 2, 1)), spec)
+    q = _as_int8_llr(arr.astype(np.float16).astype(np.float64))
+    torch = _torch()
+    dev = torch.from_numpy(np.ascontiguousarray(np.transpose(q, (0, 2, 1)))).cuda()  # (F, N, B)
+    bits, metric, ops = _matrix_frames_device(dev, spec, config)
     counter = TileOpCounter()
-    if config.radix == 2:
-        counter.mma_ops = t2 * n
-        counter.survivor_write_passes = n
-    else:
-        counter.mma_ops = t4 * (n // 2) + t2 * (n % 2)
-        counter.survivor_write_passes = n // 2 + n % 2
+    counter.mma_ops = ops
+    counter.survivor_write_passes = n // 2 + n % 2 if config.radix == 4 else n
     counter.stages = n
-    return MatrixDecodeResult(bits=bits, final_metric=metric.astype(np.float64), counter=counter)
+    return MatrixDecodeResult(bits=bits.cpu().numpy(), final_metric=metric.cpu().numpy(), counter=counter)
+
+
+def _matrix_frames_device(dev_fnb, spec: CodeSpec, config: DecoderConfig, stream=None):
+    """Tile decoder on a device (F, N, B) int8 batch -> (bits (F, N) uint8, final metric
+    float64 (F,)) device tensors and the tile ops issued per frame."""
+    torch = _torch()
+    from . import tiles
+    f, n, _ = dev_fnb.shape
+    code = _code(spec)
+    r2, _ = tiles.device_program(spec, 2)
+    r4 = tiles.device_program(spec, 4, config.optimized)[0] if config.radix == 4 else None
+    steps = n // 2 + n % 2 if config.radix == 4 else n
+    s = spec.num_states
+    kw = {"device": dev_fnb.device}
+    surv = torch.empty((f, steps, s), dtype=torch.uint8, **kw)
+    lam = torch.empty((f, s), dtype=torch.float32, **kw)
+    off = torch.empty(f, dtype=torch.float64, **kw)
+    bits = torch.empty((f, n), dtype=torch.uint8, **kw)
+    metric = torch.empty(f, dtype=torch.float64, **kw)
+    count = torch.zeros(1, dtype=torch.int64, **kw)
+    check(lib().vt_matrix_forward(ctypes.byref(code), _ptr(dev_fnb.contiguous()), f, n, ctypes.byref(r2),
+                                  ctypes.byref(r4) if r4 is not None else None, config.radix,
+                                  int(config.policy.accumulator == "half"), int(config.renormalize), _ptr(surv),
+                                  _ptr(lam), _ptr(off), _ptr(bits), _ptr(metric), _ptr(count), _stream_ptr(stream)))
+    return bits, metric, int(count.item()) // (2 * f)  # two mma.sync m16n8k16 per 16x16x16 tile op
 
 
 def decode_matrix(frame, spec: CodeSpec, config: DecoderConfig | None = None) -> MatrixDecodeResult:

@@ -31,7 +31,8 @@ from vitertile.channel import ChannelModel, generate_bits, modulate_awgn, run_po
 from vitertile.codes import (CodeSpec, compute_bomat, encode_batch, find_dragonfly_groups,  # noqa: E402
                              identical_bomat_classes)
 from vitertile.framing import decode_stream, plan_frames  # noqa: E402
-from vitertile.matrix import pack_radix4  # noqa: E402
+from vitertile.matrix import DecoderConfig, decode_matrix_batch, pack_radix4  # noqa: E402
+from vitertile.tile import PrecisionPolicy  # noqa: E402
 from vitertile.reference import decode_batch  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_r2.npz")
@@ -93,6 +94,31 @@ def main():
         frames = rng.integers(-128, 128, size=(5, b, 77)).astype(np.float64)
         bits, metric = decode_batch(frames, spec)
         add("batch", code=name, llr=frames.astype(np.int8), bits=bits, metric=metric)
+
+    # --- the tile decoder with the half accumulator (tile.py:87-89) and long frames whose
+    #     binary16 metrics overflow to inf, plus single precision on codes not in golden.npz
+    for name, (k, polys) in {**STD_CODES, "k7r2s": JIT_CODES["k7r2s"], "k5x": JIT_CODES["k5x"]}.items():
+        spec = spec_of(k, polys)
+        b = spec.outputs_per_bit
+        for n, scale in ((41, 127), (200, 40), (700, 127)):
+            frames = np.clip(np.rint(rng.normal(0, scale / 2, size=(3, b, n))), -128, 127)
+            for radix in (2, 4):
+                if radix == 4 and 2 * b > 4:
+                    continue
+                for opt in ((False, True) if radix == 4 else (False,)):
+                    for acc in ("half", "single"):
+                        for renorm in (False, True):
+                            if acc == "single" and (n != 200 or not renorm):
+                                continue
+                            cfg = DecoderConfig(radix=radix, optimized=opt, renormalize=renorm,
+                                                policy=PrecisionPolicy(accumulator=acc))
+                            with np.errstate(all="ignore"):
+                                res = decode_matrix_batch(frames, spec, cfg)
+                            add("tile", code=name, n=n, radix=radix, optimized=opt, accumulator=acc,
+                                renormalize=renorm, llr=frames.astype(np.int8), bits=res.bits,
+                                metric=np.asarray(res.final_metric, dtype=np.float64),
+                                counter=np.array([res.counter.mma_ops, res.counter.survivor_write_passes,
+                                                  res.counter.stages]))
 
     # --- dragonfly structures (radix-2 and radix-4)
     for name, (k, polys) in STD_CODES.items():

@@ -176,3 +176,23 @@ def test_foreign_frame_plan_is_recognised_by_geometry():
     ws[1] = ForeignWindow(ws[1].start + 1, ws[1].stop, ws[1].emit_start, ws[1].emit_stop)
     assert not _closed_form_plan(ForeignPlan(1000, 256, 42, tuple(ws)))
     assert not _closed_form_plan(ForeignPlan(1000, 256, 42, tuple(ws[:-1])))
+
+
+R2_TILE, _ = _r2("tile")
+
+
+@pytest.mark.parametrize("case", R2_TILE[::4], ids=[f"{c['code']}-n{c['n']}-r{c['radix']}{'o' if c['optimized'] else ''}"
+                                                    f"-{c['accumulator']}-{int(c['renormalize'])}" for c in R2_TILE[::4]])
+def test_tile_tables_model_matches_reference(z2, case):
+    """The host tile tables (tiles.py, pack_radix2/4 restated) in their per-lane
+    mma.sync fragment form, run through a numpy model of vt_tiles.cu, reproduce the
+    reference's decode_matrix_batch incl. accumulator="half" (binary16 rounding of every
+    tile result, overflow to inf on long frames) and the tile-op counter."""
+    import tile_model
+    k, gens = code_params(R2_CODES, case["code"])
+    spec = vt.CodeSpec(k, gens)
+    bits, metric, ops = tile_model.decode(z2[case["key"] + "_llr"].astype(np.int64), spec, case["radix"],
+                                          case["optimized"], case["accumulator"] == "half", case["renormalize"])
+    np.testing.assert_array_equal(bits, z2[case["key"] + "_bits"])
+    np.testing.assert_array_equal(metric, z2[case["key"] + "_metric"])
+    assert ops == int(z2[case["key"] + "_counter"][0])
