@@ -128,6 +128,17 @@ class Gen16:
         if self.pbr:  # a body's words start anywhere in the row: 15 + CH*B bytes + one word of lookahead
             self.NL = -(-(15 + self.CH * self.B + 4) // 16)
         self.lines: list[str] = []
+        # L2 policy of the history stores: the oldest quarter of the stored groups (lowest gs,
+        # longest lifetime) evict-first, the rest evict-last.  The live history set (~1 tile
+        # slot per CTA, 242 MB at config 2) exceeds L2 whatever the split; the
+        # split measured -5% DRAM bytes and +1% speed (167.3 vs 165.6 Gbps, 2 runs each).
+        self.EF = int(os.environ.get("VT_EF16", "64" if self.cheap_candidate() else "0"))  # 1/256 of the stored groups
+        # Traceback ring depth (groups prefetched ahead): 4.  8 (fits two CTAs per SM for K=7
+        # r1/2) measured 165.2 vs 167.4 Gbps at 2^20 windows, 123.5 vs 120.0 at 2^16 (the
+        # CTA's last-tile traceback is latency-bound) -- VT_TBD16 overrides.
+        if not tc and "VT_TBD16" in os.environ:
+            self.TBD = int(os.environ["VT_TBD16"])
+            assert self.TBD in (2, 4, 8, 16)
         ring = self.TBD * (self.S // 16)
         # row stride (uint4) of the per-thread LLR rows: odd, so the realignment's 4-byte loads
         # (the same byte offset in every thread's row) spread over 8 bank groups (4-way) instead
@@ -146,6 +157,11 @@ class Gen16:
             self.TCN = self.CH * 4           # MMA N: 4 pattern sums per stage of a chunk
             self.TCOFF = self.SMEM           # A tiles [buffer][window set] 4 KB each, B 2 KB, barriers
             self.SMEM += 4 * 4096 + 2048 + 64
+
+    def cheap_candidate(self) -> bool:
+        """K=7 rate 1/2 (the cheap-middle-stage form): the evict-first history split helps it
+        (+0.9%) and costs K=7 r1/3 0.7%."""
+        return self.B == 2 and self.K == 7
 
     def pattern(self, i: int, u: int) -> int:
         reg = (u << self.k) | i
@@ -406,6 +422,8 @@ class Gen16:
         e(f"{ind}if (gidx >= a.b_lo) {{")
         e(f"{ind}  const int gs = gidx - a.b_lo;")
         e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {S // 16} * {NT};")
+        if self.EF:
+            e(f"{ind}  const uint64_t pol_h = gs < ef_lim ? pol_first : pol_last;")
         for j in range(S):
             e(f"{ind}  const uint32_t h{j} = m{j} & {hm:#x}u;")
         words = []
@@ -416,7 +434,8 @@ class Gen16:
             words.append(acc)
         for g in range(S // 16):
             ws = ", ".join(words[4 * g: 4 * g + 4])
-            e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), pol_last);")
+            pol = "pol_h" if self.EF else "pol_last"
+            e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), {pol});")
         if not self.xmin:  # IMAD clear (FMA pipe): the ALU pipe is the K=7 r1/2 bottleneck
             for j in range(S):
                 e(f"{ind}  m{j} = vt::mad_u32(h{j}, 0xFFFFFFFFu, m{j});")
@@ -458,6 +477,10 @@ class Gen16:
         e(f"  uint4* const s_tb = smem_dyn + {4 * self.RS * NT};  // (even GPB only)")
         e("  (void)s_tb;")
         e("  const uint64_t pol_last = vt::policy_evict_last();")
+        if self.EF:
+            e("  const uint64_t pol_first = vt::policy_evict_first();")
+        if self.EF:
+            e(f"  const int ef_lim = (a.nbs * {self.EF}) >> 8;  // stored groups gs < ef_lim: evict-first")
         if self.tma:
             e(f"  uint64_t* const s_bar = reinterpret_cast<uint64_t*>(smem_dyn + {self.SMEM_TMA_OFF // 16});  // TMA chunk barriers [warp][buffer]")
             e("  const int warp = tid >> 5, lane = tid & 31;")

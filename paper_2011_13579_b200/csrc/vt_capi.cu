@@ -186,7 +186,24 @@ int prepare(const KernelEntry* k) {
     cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem);
     if (k->fn_nofm) cudaFuncSetAttribute(k->fn_nofm, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem);
   }
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->nt, k->smem) != cudaSuccess || occ < 1) occ = 1;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->fn, k->nt, k->smem);
+  if (getenv("VT_DEBUG_OCC")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k->fn);
+    fprintf(stderr, "[vt] occupancy K=%d tc=%d: %d CTAs/SM (err %d, regs %d, static smem %zu, dyn %d, max dyn %d)\n", k->K,
+            k->tc, occ, (int)e, fa.numRegs, fa.sharedSizeBytes, k->smem, fa.maxDynamicSharedSizeBytes);
+  }
+  if (e != cudaSuccess || occ < 1) occ = 1;
+  if (k->tc && e == cudaSuccess) {
+    // The occupancy query answers 1 for the tcgen05 kernels although two CTAs fit (256 TMEM
+    // columns each, 2 x ~77 KB shared memory, <= 240 registers): size by those limits.
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, k->fn) == cudaSuccess && fa.numRegs > 0) {
+      const int by_regs = 65536 / (((fa.numRegs + 7) / 8) * 8 * k->nt);
+      const int by_smem = (228 * 1024) / (k->smem + (int)fa.sharedSizeBytes + 1024);
+      occ = std::max(occ, std::min({by_regs, by_smem, 2}));
+    }
+  }
   return occ;
 }
 

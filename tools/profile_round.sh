@@ -11,4 +11,4 @@ ncu --set full --clock-control none --import-source on -k regex:vtk16 -s 3 -c 1 
 python tools/ncu_summary.py gpurun_out/prof_k16.ncu-rep > gpurun_out/ncu_k16_summary.txt 2>&1
 ncu -i gpurun_out/prof_k16.ncu-rep --page source --csv --print-source sass > gpurun_out/k16_source.csv 2>/dev/null
 python tools/sass_hist.py gpurun_out/k16_source.csv --regions --stalls > gpurun_out/k16_sass_hist.txt 2>&1
-./tools/acsbench/acsbench > gpurun_out/acsbench.jsonl 2>&1
+make -s -C tools/acsbench && ./tools/acsbench/acsbench > gpurun_out/acsbench.jsonl 2>&1
