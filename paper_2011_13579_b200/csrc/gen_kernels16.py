@@ -132,6 +132,13 @@ class Gen16:
         # longest lifetime) evict-first, the rest evict-last.  The live history set (~1 tile
         # slot per CTA, 242 MB at config 2) exceeds L2 whatever the split; the
         # split measured -5% DRAM bytes and +1% speed (167.3 vs 165.6 Gbps, 2 runs each).
+        # VT_SEED16: semantically neutral emission choices (butterfly order of the full
+        # stages, traceback step before/after the history store).  ptxas's schedule -- the
+        # issue efficiency, 67-72% -- depends on them: seeds 1-8 measured 161.1-167.4 Gbps,
+        # the default order (0) 167.4
+        self.seed = int(os.environ.get("VT_SEED16", "0"))
+        import random
+        self.rng = random.Random(self.seed)
         self.EF = int(os.environ.get("VT_EF16", "64" if self.cheap_candidate() else "0"))  # 1/256 of the stored groups
         # Traceback ring depth (groups prefetched ahead): 4.  8 (fits two CTAs per SM for K=7
         # r1/2) measured 165.2 vs 167.4 Gbps at 2^20 windows, 123.5 vs 120.0 at 2^16 (the
@@ -220,7 +227,10 @@ class Gen16:
             e(f"{ind}const uint32_t U{q}_{b} = vt::vadd2(P{q}_{b}, 0x00800080u) << {L};")
             e(f"{ind}const uint32_t N{q}_{b} = {(256 << L) * 0x10001:#x}u - U{q}_{b};")
         outs, body, need_d, need_e = [None] * S, [], set(), set()
-        order = [x for k in range(S // 2) for x in (k, k + S // 2)]
+        ks = list(range(S // 2))
+        if self.seed and not (self.cheap and gq in (1, 2)):
+            self.rng.shuffle(ks)
+        order = [x for k in ks for x in (k, k + S // 2)]
         if self.cheap and gq == 1:
             # CHEAP stage: with the i0 branch metric as a per-state offset phi_j of the
             # stored metric (stored = true - S(p0(j))), the update needs no candidate add:
@@ -418,7 +428,9 @@ class Gen16:
         e(f"{ind}}}")
         e(f"{ind}// one traceback step per window of the previous tile (fields prefetched two groups")
         e(f"{ind}// ahead: the 2^L candidate states of a group are consecutive)")
-        self.tb_step_both(ind, ge % 2)
+        tb_after = bool(self.seed) and self.rng.random() < 0.5
+        if not tb_after:
+            self.tb_step_both(ind, ge % 2)
         e(f"{ind}if (gidx >= a.b_lo) {{")
         e(f"{ind}  const int gs = gidx - a.b_lo;")
         e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {S // 16} * {NT};")
@@ -443,6 +455,8 @@ class Gen16:
         if self.xmin:  # r1/3: unconditional LOP3 clear, no phi moves (128.4 vs 127.3 Gbps)
             for j in range(S):
                 e(f"{ind}m{j} &= {lm:#x}u;")
+        if tb_after:
+            self.tb_step_both(ind, ge % 2)
         e(f"{ind}++gidx;")
 
     def kernel(self) -> str:
