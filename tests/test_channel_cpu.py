@@ -60,3 +60,31 @@ def test_csv(tmp_path):
     p = tmp_path / "ber.csv"
     ch.write_ber_csv([ch.BerPoint(3.0, 10, 1, 0.1, False)], str(p))
     assert p.read_text().splitlines()[1].startswith("3.0,10,1,0.1,0")
+
+
+def test_csv_bytes_match_the_reference_writer(tmp_path):
+    """Byte-identical to the reference's csv.writer rows (channel.py:168-173: CRLF
+    dialect, ber formatted %.6g)."""
+    import csv
+    pts = [ch.BerPoint(2.5, 1000000, 1234, 0.001234, True), ch.BerPoint(3.0, 10, 1, 0.1, False),
+           ch.BerPoint(0.25, 7, 0, 0.0, True)]
+    want = tmp_path / "want.csv"
+    with open(want, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["ebn0_db", "n", "errors", "ber", "valid"])
+        for p in pts:
+            w.writerow([p.ebn0_db, p.n, p.errors, f"{p.ber:.6g}", int(p.valid)])
+    got = tmp_path / "got.csv"
+    ch.write_ber_csv(pts, str(got))
+    assert got.read_bytes() == want.read_bytes()
+
+
+def test_ebn0_at_ber_first_crossing_and_flat_segment():
+    pts = [ch.BerPoint(0.0, 10, 5, 0.5, True), ch.BerPoint(1.0, 10, 1, 0.1, True),
+           ch.BerPoint(2.0, 10, 1, 0.1, True), ch.BerPoint(3.0, 10, 0, 0.0, True),
+           ch.BerPoint(4.0, 100, 1, 0.01, True)]
+    assert ch.ebn0_at_ber(pts, 0.1) == 1.0          # first bracketing pair, ber_lo == target
+    assert ch.ebn0_at_ber(pts[1:3], 0.1) == 1.0     # flat segment
+    # the 3.0 dB point has no errors: the crossing of 0.05 lies between 2.0 dB and 4.0 dB
+    t = (np.log(0.1) - np.log(0.05)) / (np.log(0.1) - np.log(0.01))
+    assert ch.ebn0_at_ber(pts, 0.05) == pytest.approx(2.0 + 2.0 * t, abs=1e-12)
