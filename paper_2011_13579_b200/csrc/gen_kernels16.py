@@ -40,6 +40,12 @@ CH_BODIES = 2  # loop bodies per LLR chunk
 MINB16 = 1  # CTAs per SM bound (3 forces a 168-register cap: spills, measured 16% slower with the ring traceback)
 
 
+# Emission seeds picked by measurement (tools/_gpu_var.sh over VT_SEED16 / VT_SEED16M = 0..7,
+# 2^28 stages, profiles/r2_schedule_sweep.txt): K=7 r1/3 seed 5 130.7 vs 129.3 Gbps,
+# K=9 seed 7 33.52 vs 33.37; K=7 r1/2 keeps the default order (the fastest of 13).
+MEASURED_SEEDS = {(7, (0o133, 0o171, 0o165)): 5, (9, (0o753, 0o561)): 7}
+
+
 def history_bits(K: int, B: int) -> int:
     dmax = 128 * B
     sb = 2 * (K - 1) * dmax
@@ -136,7 +142,7 @@ class Gen16:
         # stages, traceback step before/after the history store).  ptxas's schedule -- the
         # issue efficiency, 67-72% -- depends on them: seeds 1-8 measured 161.1-167.4 Gbps,
         # the default order (0) 167.4
-        self.seed = int(os.environ.get("VT_SEED16", "0"))
+        self.seed = int(os.environ.get("VT_SEED16", str(MEASURED_SEEDS.get((K, tuple(gens)), 0))))
         import random
         self.rng = random.Random(self.seed)
         self.EF = int(os.environ.get("VT_EF16", "64" if self.cheap_candidate() else "0"))  # 1/256 of the stored groups

@@ -28,7 +28,7 @@ from __future__ import annotations
 import os
 
 from gen_kernels import parity
-from gen_kernels16 import Gen16, history_bits, spread_weight
+from gen_kernels16 import MEASURED_SEEDS, Gen16, history_bits, spread_weight
 
 NT = 128  # threads per CTA
 
@@ -80,6 +80,11 @@ class Gen16M(Gen16):
         self.SM_X = self.NPAIR * self.XS * 4
         self.SMEM = self.SM_LLR + self.SM_RING + self.SM_X
         self.lines: list[str] = []
+        # neutral emission choices (as Gen16's VT_SEED16): butterfly order of the full
+        # stages, traceback step before/after the history store
+        import random
+        self.seed = int(os.environ.get("VT_SEED16M", str(MEASURED_SEEDS.get((K, tuple(gens)), 0))))
+        self.rng = random.Random(self.seed)
 
     # state <-> (lane, slot) for a partition at bits [lo, lo+tau)
     def slot_of(self, s: int, lo: int) -> int:
@@ -121,7 +126,10 @@ class Gen16M(Gen16):
                 e(f"{ind}const uint32_t U{q}_{b} = (u{q}_{b} & ~{m}) | (n{q}_{b} & {m});")
                 e(f"{ind}const uint32_t N{q}_{b} = (n{q}_{b} & ~{m}) | (u{q}_{b} & {m});")
         outs, body, need_d, need_e = [None] * SL, [], set(), set()
-        order = [x for k in range(SL // 2) for x in (k, k + SL // 2)]
+        ks = list(range(SL // 2))
+        if self.seed and not (self.cheap and gq in (1, 2)):
+            self.rng.shuffle(ks)
+        order = [x for k in ks for x in (k, k + SL // 2)]
         full = (1 << B) - 1
 
         def preds(r):
@@ -285,7 +293,9 @@ class Gen16M(Gen16):
             e(f"{ind}  pendA = (int64_t)((r0 & 0xFFFFu) >> {L}) - {self.Sb};")
             e(f"{ind}  pendB = (int64_t)(r0 >> {16 + L}) - {self.Sb};")
         e(f"{ind}}}")
-        self.tb_step(ind)
+        tb_after = bool(self.seed) and self.rng.random() < 0.5
+        if not tb_after:
+            self.tb_step(ind)
         e(f"{ind}if (gidx >= a.b_lo) {{")
         e(f"{ind}  const int gs = gidx - a.b_lo;")
         e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {SQ} * {NT};")
@@ -304,6 +314,8 @@ class Gen16M(Gen16):
         # clear unconditionally (warm-up groups carry no decision bits): no phi moves
         for r in range(SL):
             e(f"{ind}m{r} &= {lm:#x}u;")
+        if tb_after:
+            self.tb_step(ind)
         e(f"{ind}++gidx;")
 
     def exchange_write(self, ind: str, lo: int) -> None:
