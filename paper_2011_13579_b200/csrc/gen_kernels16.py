@@ -145,6 +145,12 @@ class Gen16:
         self.seed = int(os.environ.get("VT_SEED16", str(MEASURED_SEEDS.get((K, tuple(gens)), 0))))
         import random
         self.rng = random.Random(self.seed)
+        # last-tile traceback 8 groups deep through the freed LLR rows (needs TBD = 4 and rows
+        # of >= 4 ring entries).  Measured (2^24 / 2^26 / 2^28 stages): r1/3 +2.5% / - / +0.1%;
+        # r1/2 +2.4% / -1.0% / -0.6% (ptxas reallocates the body's registers), so r1/3 only
+        self.DRAIN8 = (self.pbr and os.environ.get("VT_DRAIN8", "0" if self.cheap_candidate() else "1") == "1"
+                       and 4 * ((-(-(15 + self.P * int(os.environ.get("VT_CHB16", "5")) * self.B + 4) // 16)) | 1)
+                       >= 4 * (self.S // 16) and "VT_TBD16" not in os.environ)
         self.EF = int(os.environ.get("VT_EF16", "64" if self.cheap_candidate() else "0"))  # 1/256 of the stored groups
         # Traceback ring depth (groups prefetched ahead): 4.  8 (fits two CTAs per SM for K=7
         # r1/2) measured 165.2 vs 167.4 Gbps at 2^20 windows, 123.5 vs 120.0 at 2^16 (the
@@ -357,6 +363,57 @@ class Gen16:
         for q in range(SQ):
             e(f"{ind}  vt::cp_async16(dst + {q * NT}, slotc + xo + {q * NT * 16}u, 16, 0);")
         e(f"{ind}  vt::cp_async_commit();")
+        e(f"{ind}}}")
+
+    def drain_entry(self, r: str) -> str:
+        """Ring entry r (0..7) of the last-tile drain: 0-3 the traceback ring, 4-7 the LLR row
+        buffers (free once the CTA's last forward pass is done)."""
+        SQ = self.S // 16
+        return f"(({r}) < 4 ? s_tb + ({r}) * {SQ * NT} : s_llr + (({r}) - 4) * {SQ * NT}) + tid"
+
+    def drain_last_tile(self, ind: str) -> None:
+        """Traceback of the CTA's last tile, alone after the forward passes: latency-bound on
+        the history fetches, so it prefetches 8 groups deep (the 4-entry ring + 4 entries in
+        the LLR row buffers) instead of 4.  The prefill left groups tbb..tbb-3 in entries 0-3."""
+        S, SQ, L = self.S, self.S // 16, self.L
+        fm = (1 << L) - 1
+        e = self.emit
+        e(f"{ind}__syncthreads();  // every warp is done with its LLR rows (entries 4-7 span all threads' rows)")
+        e(f"{ind}for (int r = 4; r < 8; ++r) {{  // groups tbb-4 .. tbb-7 -> entries 4-7")
+        e(f"{ind}  const uint32_t xo = (uint32_t)(txa + txs * max(tbb - r, a.b_lo)) * {SQ * NT * 16}u;")
+        e(f"{ind}  uint4* const dst = {self.drain_entry('r')};")
+        for q in range(SQ):
+            e(f"{ind}  vt::cp_async16(dst + {q * NT}, slotc + xo + {q * NT * 16}u, 16, 0);")
+        e(f"{ind}  vt::cp_async_commit();")
+        e(f"{ind}}}")
+        e(f"{ind}int dr = 0;  // drain ring entry of group tbb")
+        e(f"{ind}while (tbb >= a.b_lo) {{")
+        e(f"{ind}#pragma unroll")
+        e(f"{ind}  for (int u = 0; u < 2; ++u) {{")
+        e(f"{ind}    vt::cp_async_wait_group<7>();")
+        e(f"{ind}    const char* const rs = reinterpret_cast<const char*>({self.drain_entry('dr')});")
+        for w, side in (("A", 0), ("B", 16)):
+            e(f"{ind}    {{")
+            e(f"{ind}      const uint32_t j = tb{w}.j;")
+            e(f"{ind}      const uint32_t wd = *reinterpret_cast<const uint32_t*>(rs + ((j & 48u) << 7) + (j & 12u));")
+            e(f"{ind}      const uint32_t h = (wd >> ((j & 3u) * {L}u + {side}u)) & {fm}u;")
+            e(f"{ind}      tb{w}.acc = (tb{w}.acc << {L}) | (j >> {self.k - L});")
+            e(f"{ind}      tb{w}.j = ((j << {L}) | h) & {S - 1}u;")
+            e(f"{ind}      tb{w}.lo -= {L};")
+            e(f"{ind}      --tb{w}.b;")
+            e(f"{ind}    }}")
+        e(f"{ind}    --tbb;")
+        e(f"{ind}    {{")
+        e(f"{ind}      const uint32_t xo = (uint32_t)(txa + txs * max(tbb - 7, a.b_lo)) * {SQ * NT * 16}u;")
+        e(f"{ind}      uint4* const dst = {self.drain_entry('dr')};")
+        for q in range(SQ):
+            e(f"{ind}      vt::cp_async16(dst + {q * NT}, slotc + xo + {q * NT * 16}u, 16, 0);")
+        e(f"{ind}      vt::cp_async_commit();")
+        e(f"{ind}    }}")
+        e(f"{ind}    dr = (dr + 1) & 7;")
+        e(f"{ind}  }}")
+        e(f"{ind}  tbA.settle(a);")
+        e(f"{ind}  tbB.settle(a);")
         e(f"{ind}}}")
 
     def tb_step_both(self, ind: str, p: int = 0) -> None:
@@ -818,12 +875,15 @@ class Gen16:
             self.tb_fetch("    ", f"tbb - {r}", f"{r}")
         e("  }")
         e("  // traceback of the CTA's last tile")
-        e("  while (tbb >= a.b_lo) {")
-        self.tb_step_both("    ", 0)
-        self.tb_step_both("    ", 1)
-        e("    tbA.settle(a);")
-        e("    tbB.settle(a);")
-        e("  }")
+        if self.DRAIN8:
+            self.drain_last_tile("  ")
+        else:
+            e("  while (tbb >= a.b_lo) {")
+            self.tb_step_both("    ", 0)
+            self.tb_step_both("    ", 1)
+            e("    tbA.settle(a);")
+            e("    tbB.settle(a);")
+            e("  }")
         e("  tbA.b = tbB.b = tbb;")
         e("  if (tbA.running) tbA.drain_unstored(a);")
         e("  if (tbB.running) tbB.drain_unstored(a);")
