@@ -55,20 +55,81 @@ def history_bits(K: int, B: int) -> int:
     raise ValueError("no history width fits")
 
 
+def weight_table(K: int, gens: tuple[int, ...]) -> list[int]:
+    """w[e] = Hamming weight of the encoder output of the K-1 input bits e from the zero
+    state (newest bit at the register MSB as codes.py:183-193).  Two paths from one
+    state that end in states s and s' (s' = s ^ e: the end state is the last K-1 inputs)
+    differ in at most w[e] output bits, so |Lambda(s) - Lambda(s')| <= 256 * w[e] for
+    |l| <= 128 -- at every stage, also inside the window's first K-1 stages (all initial
+    metrics are equal) and over zero-LLR padding."""
+    k = K - 1
+    out = []
+    for e in range(1 << k):
+        reg, w = 0, 0
+        for t in range(k):
+            reg = (reg >> 1) | (((e >> t) & 1) << k)
+            w += sum(parity(g & reg) for g in gens)
+        out.append(w)
+    return out
+
+
 def spread_weight(K: int, gens: tuple[int, ...]) -> int:
     """Max Hamming weight of the output difference of two K-1-stage paths from the same
     state (= encoder output weight of a nonzero input sequence from the zero state,
     newest bit at the register MSB as codes.py:183-193): the metric spread is at most
     256 * this for |l| <= 128."""
-    k = K - 1
-    best = 0
-    for e in range(1, 1 << k):
-        reg, w = 0, 0
-        for t in range(k):
-            reg = (reg >> 1) | (((e >> t) & 1) << k)
-            w += sum(parity(g & reg) for g in gens)
-        best = max(best, w)
-    return best
+    return max(weight_table(K, gens))
+
+
+_RSET_CACHE: dict = {}
+
+
+def renorm_set(K: int, gens: tuple[int, ...], wmax: int, allowed=None, max_size: int = 6,
+               budget: int = 300000):
+    """Smallest state set T (|T| <= max_size, members from `allowed`) whose minimum metric
+    is within 256 * W_T of the exact minimum, W_T = max_m min_{t in T} w[t ^ m] <= wmax
+    (weight_table's bound applied to the minimising state m and its nearest member of T).
+    Renormalising by R = min_T Lambda - 256 * W_T then keeps every metric in
+    [0, 256 * W_T + Delta] at a group start, like the exact minimum up to 256 * W_T, for
+    |T| - 1 min operations instead of a tree over all states.  Set cover by depth-first
+    search (branch on the lowest uncovered state).  Returns (sorted T, W_T) or None."""
+    key = (K, tuple(gens), wmax, None if allowed is None else tuple(sorted(allowed)), max_size)
+    if key in _RSET_CACHE:
+        return _RSET_CACHE[key]
+    S = 1 << (K - 1)
+    w = weight_table(K, gens)
+    full = (1 << S) - 1
+    pool = set(range(S)) if allowed is None else set(allowed)
+    ball = [e for e in range(S) if w[e] <= wmax]
+    cover = {t: sum(1 << (t ^ e) for e in ball) for t in pool}
+    nodes = [0]
+
+    def dfs(cov: int, n: int, T: list):
+        nodes[0] += 1
+        if cov == full:
+            return T
+        if n == 0 or nodes[0] > budget:
+            return None
+        free = ~cov & full
+        m = (free & -free).bit_length() - 1
+        for e in ball:
+            t = m ^ e
+            if t in cover:
+                r = dfs(cov | cover[t], n - 1, T + [t])
+                if r is not None:
+                    return r
+        return None
+
+    res = None
+    for n in range(1, max_size + 1):
+        nodes[0] = 0
+        r = dfs(0, n, [])
+        if r is not None:
+            T = sorted(r)
+            res = (T, max(min(w[t ^ m] for t in T) for m in range(S)))
+            break
+    _RSET_CACHE[key] = res
+    return res
 
 
 class Gen16:
@@ -122,8 +183,21 @@ class Gen16:
         # measured slower than the plain stage: 120.0 vs 123.6 Gbps for K=7 r1/3)
         self.cheap = (not self.xmin and self.L == 3 and self.supported and comp and
                       sbc + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)))
-        if self.xmin:  # the minimum renormalises to 0
-            self.Sb = 0
+        # Subset minimum (round 2): renormalise by the minimum over a small state set T
+        # (renorm_set) instead of the exact minimum over all 2^(K-1) states: the metrics
+        # then span [0, Sb' + Delta] with Sb' = 256 * W_T at a group start, which must still
+        # leave L stages of growth below 2^(16-L).  K=7 r1/3: |T| = 6, W_T = 7 (7936 < 8192):
+        # 3 VIMNMX instead of a 32-instruction tree per group.  VT_RSET=0: the exact minimum.
+        self.rset = None
+        if self.xmin and os.environ.get("VT_RSET", "1") == "1":
+            wmax = ((1 << (16 - L)) - 1 - delta - L * 2 * self.dmax) // 256
+            r = renorm_set(K, gens, wmax) if wmax >= 0 else None
+            if r is not None:
+                self.rset = r[0]
+                self.Sb_rset = 256 * r[1]
+        if self.xmin:  # the minimum renormalises to 0 (the subset minimum to Sb' = 256 * W_T)
+            self.Sb = self.Sb_rset if self.rset else 0
+            assert self.Sb + delta + L * 2 * self.dmax < (1 << (16 - L)), "metric range"
         elif self.cheap:
             self.Sb = sbc
         self.NWC = -(-self.CH * self.B // 4)
@@ -459,9 +533,9 @@ class Gen16:
             e(f"{ind}offA += pendA;")
             e(f"{ind}offB += pendB;")
         e(f"{ind}{{")
-        if self.xmin:  # exact per-half minimum over all states (history bits masked after)
+        if self.xmin:  # per-half minimum over all states or over the set rset (history bits masked after)
             # ternary tree min(min(a, b), c): ptxas fuses each into one VIMNMX3.U16x2
-            vals = [f"m{j}" for j in range(S)]
+            vals = [f"m{j}" for j in (self.rset if self.rset else range(S))]
             lvl = 0
             while len(vals) > 1:
                 nxt = []

@@ -28,7 +28,7 @@ from __future__ import annotations
 import os
 
 from gen_kernels import parity
-from gen_kernels16 import MEASURED_SEEDS, Gen16, history_bits, spread_weight
+from gen_kernels16 import MEASURED_SEEDS, Gen16, history_bits, renorm_set, spread_weight
 
 NT = 128  # threads per CTA
 
@@ -63,6 +63,27 @@ class Gen16M(Gen16):
                    for j in range(self.S))
         self.cheap = (os.environ.get("VT_CHEAP16M", "0") == "1" and comp and self.B == 2)  # measured 31.1 vs 31.5 Gbps (K=9)
         self.Sb = 2 * self.dmax if self.cheap else 0
+        # Subset minimum (round 2, gen_kernels16.renorm_set): at group end ge (partition
+        # lo = top - L*(ge+1)) renormalise by the minimum over a state set T_ge that lives on
+        # ONE lane (min over its slots there + one shuffle from that lane) instead of the
+        # per-lane tree over all 64 slots + 2 xor shuffles.  K=9 (753,561): T = {0, 193} /
+        # {0, 4}, W_T = 9 / 10, Sb' = 2560: 2560 + 3328 + 3*512 = 7424 < 8192.
+        self.rsets = None
+        self.GPB = self.P // self.L
+        if not self.cheap and os.environ.get("VT_RSET", "1") == "1":
+            wmax = ((1 << (16 - self.L)) - 1 - delta - self.L * 2 * self.dmax) // 256
+            found = []
+            for ge in range(self.GPB):
+                lo = self.top - self.L * (ge + 1)
+                best = None
+                for lane in range(T):
+                    r = renorm_set(K, gens, wmax, allowed=[self.state_of(x, lane, lo) for x in range(self.SL)])
+                    if r is not None and (best is None or (len(r[0]), r[1]) < (len(best[0]), best[1])):
+                        best = (r[0], r[1], lane)
+                found.append(best)
+            if all(f is not None for f in found):
+                self.rsets = found
+                self.Sb = 256 * max(f[1] for f in found)
         assert self.Sb + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)), "metric range"
         self.pbr = True
         self.tc = False
@@ -259,12 +280,20 @@ class Gen16M(Gen16):
         e = self.emit
         hm = ((1 << L) - 1) * 0x10001
         lm = (0xFFFF & ~((1 << L) - 1)) * 0x10001
-        e(f"{ind}// ---- group end: renormalise by the exact per-half minimum over all lanes")
+        if self.rsets:
+            e(f"{ind}// ---- group end: renormalise by the per-half minimum over the state set T (one lane)")
+        else:
+            e(f"{ind}// ---- group end: renormalise by the exact per-half minimum over all lanes")
         if self.fm:
             e(f"{ind}offA += pendA;")
             e(f"{ind}offB += pendB;")
         e(f"{ind}{{")
-        vals = [f"m{r}" for r in range(SL)]
+        if self.rsets:
+            Tset, _, owner = self.rsets[ge]
+            lo = self.top - L * (ge + 1)
+            vals = [f"m{self.slot_of(x, lo)}" for x in Tset]
+        else:
+            vals = [f"m{r}" for r in range(SL)]
         lvl = 0
         while len(vals) > 1:
             nxt = []
@@ -283,8 +312,11 @@ class Gen16M(Gen16):
                 i += 3
             vals, lvl = nxt, lvl + 1
         e(f"{ind}  uint32_t mn = {vals[0]};")
-        for d in range(self.tau):
-            e(f"{ind}  mn = vt::vmin2(mn, __shfl_xor_sync(pm, mn, {1 << d}));")
+        if self.rsets:  # T lives on lane `owner` of the pair at this partition
+            e(f"{ind}  mn = __shfl_sync(pm, mn, {owner}, {self.T});  // T = {{{', '.join(map(str, Tset))}}}")
+        else:
+            for d in range(self.tau):
+                e(f"{ind}  mn = vt::vmin2(mn, __shfl_xor_sync(pm, mn, {1 << d}));")
         e(f"{ind}  const uint32_t r0 = mn & {lm:#x}u;")
         e(f"{ind}  const uint32_t rr = vt::vadd2(r0, {((-(self.Sb << L)) & 0xFFFF) * 0x10001:#x}u);")
         e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);")

@@ -6,7 +6,8 @@ LLR term enters biased (U_b = (l+128) << L, N_b = (256 << L) - U_b); the i1
 candidate carries +2^q at group stage q (stored groups only); the cheap middle
 stage stores metric - S(p0) and the next stage absorbs the offsets; group ends
 mask, store and clear the L-bit fields and renormalise the next group by
-Lambda_0 - S_b or by the exact minimum (the generator's own choice); traceback
+Lambda_0 - S_b, by the exact minimum or by the minimum over a small state set
+(renorm_set; the generator's own choice); traceback
 j_prev = ((j << L) | h) & (S-1).  Every value the kernels compute in a 16-bit
 half is asserted to stay in [0, 2^16) -- the range argument of the generators,
 exercised on the CPU against the oracle and the adversarial streams.
@@ -44,6 +45,15 @@ def _in_range(x, what):
 def decode_stream_model16(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> np.ndarray:
     g = _gen(K, gens)
     L, CH, Sb, cheap, xmin = g.L, g.CH, g.Sb, g.cheap, g.xmin
+    multilane = hasattr(g, "rsets")
+    # renormalisation reference per group position in the body: all states (exact minimum),
+    # the subset T (gen_kernels16.renorm_set) or state 0
+    if multilane and g.rsets:
+        refsets = [np.array(r[0]) for r in g.rsets]
+    elif not multilane and getattr(g, "rset", None):
+        refsets = [np.array(g.rset)] * g.GPB
+    else:
+        refsets = None
     n, B = llr_nb.shape
     k = K - 1
     S = 1 << k
@@ -71,7 +81,7 @@ def decode_stream_model16(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> n
         e0, e1 = w * F, min(w * F + F, n)
         s, stop = max(0, e0 - V), min(n, e1 + V)
         g0 = stop - CH * nc
-        m = np.full(S, (Sb << L) if cheap else 0, dtype=np.int64)
+        m = np.full(S, (Sb << L) if (cheap or multilane) else 0, dtype=np.int64)
         negR = 0  # renormalisation R = Lambda_ref*2^L - Sb*2^L, subtracted in group stage 0
         fields = {}
         s_prev = None
@@ -105,7 +115,12 @@ def decode_stream_model16(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> n
                     m = np.maximum(cand0, cand1)
             # group end: renormalisation reference, fields, clear
             lm = LIM - (1 << L)
-            ref = (int(m.min()) if xmin else int(m[0])) & lm
+            if refsets is not None:
+                ref = int(m[refsets[gi % g.GPB]].min()) & lm
+                # the subset minimum is within 256 * W_T = Sb of the exact minimum
+                assert int(m.min()) & lm >= ref - (Sb << L)
+            else:
+                ref = (int(m.min()) if xmin else int(m[0])) & lm
             negR = ref - (Sb << L)
             h = m & ((1 << L) - 1)
             if gi >= b_lo:

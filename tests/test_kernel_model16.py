@@ -36,6 +36,13 @@ def test_model16_adversarial_stream_in_range(name, k, gens):
     np.testing.assert_array_equal(decode_stream_model16(q, k, gens, 256, 42), want)
 
 
+@pytest.mark.parametrize("name,k,gens", [("k7r3", 7, (0o133, 0o171, 0o165)), ("k9r2", 9, (0o753, 0o561))])
+def test_model16_adversarial_gap_stream_in_range(name, k, gens):
+    q = np.load(os.path.join(ROOT, "tests", "golden", f"adversarial_gap_{name}.npz"))["llr"][:3000]
+    want = oracle.decode_stream(q, k, gens, 256, 42, threads=4)
+    np.testing.assert_array_equal(decode_stream_model16(q, k, gens, 256, 42), want)
+
+
 def test_model16_range_check_has_teeth(monkeypatch):
     """With the renormalisation target below the spread bound (S_b' = 512 instead of
     Delta + 512) the adversarial stream drives a cheap-stage candidate negative."""
