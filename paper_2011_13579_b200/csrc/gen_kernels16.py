@@ -188,6 +188,8 @@ class Gen16:
         # then span [0, Sb' + Delta] with Sb' = 256 * W_T at a group start, which must still
         # leave L stages of growth below 2^(16-L).  K=7 r1/3: |T| = 6, W_T = 7 (7936 < 8192):
         # 3 VIMNMX instead of a 32-instruction tree per group.  VT_RSET=0: the exact minimum.
+        self.clri = int(os.environ.get("VT_CLRI16", "0"))  # xmin group end: IMAD clears (see group_end)
+        self.gebf = os.environ.get("VT_GEBF16", "0") == "1"
         self.rset = None
         if self.xmin and os.environ.get("VT_RSET", "1") == "1":
             wmax = ((1 << (16 - L)) - 1 - delta - L * 2 * self.dmax) // 256
@@ -226,6 +228,9 @@ class Gen16:
                        and 4 * ((-(-(15 + self.P * int(os.environ.get("VT_CHB16", "5")) * self.B + 4) // 16)) | 1)
                        >= 4 * (self.S // 16) and "VT_TBD16" not in os.environ)
         self.EF = int(os.environ.get("VT_EF16", "64" if self.cheap_candidate() else "0"))  # 1/256 of the stored groups
+        self.polfrac = os.environ.get("VT_POLFRAC16", "")  # e.g. "0.75": fractional evict_last/evict_first
+        if self.polfrac:
+            self.EF = 0
         # Traceback ring depth (groups prefetched ahead): 4.  8 (fits two CTAs per SM for K=7
         # r1/2) measured 165.2 vs 167.4 Gbps at 2^20 windows, 123.5 vs 120.0 at 2^16 (the
         # CTA's last-tile traceback is latency-bound) -- VT_TBD16 overrides.
@@ -568,19 +573,33 @@ class Gen16:
         tb_after = bool(self.seed) and self.rng.random() < 0.5
         if not tb_after:
             self.tb_step_both(ind, ge % 2)
-        e(f"{ind}if (gidx >= a.b_lo) {{")
-        e(f"{ind}  const int gs = gidx - a.b_lo;")
-        e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {S // 16} * {NT};")
-        if self.EF:
-            e(f"{ind}  const uint64_t pol_h = gs < ef_lim ? pol_first : pol_last;")
-        for j in range(S):
-            e(f"{ind}  const uint32_t h{j} = m{j} & {hm:#x}u;")
+        # xmin kernels (ALU-heavy: the clears are LOP3s): the fields of the first CLRI states
+        # are taken before the store branch and those states are cleared with IMADs (FMA
+        # pipe); GEBF: the whole group end (fields, packs, clears) unconditional, only the
+        # stores under the branch.  Warm-up groups carry zero fields, so both are exact.
+        pre = range(S) if (self.xmin and self.gebf) else range(self.clri if self.xmin else 0)
+        e(f"{ind}{{  // group-end scope (fields h, packs hw)")
+        for j in pre:
+            e(f"{ind}const uint32_t h{j} = m{j} & {hm:#x}u;")
         words = []
         for w in range(S // 4):
             acc = f"h{4 * w}"
             for t in range(1, 4):
                 acc = f"vt::mad_u32(h{4 * w + t}, {1 << (L * t)}u, {acc})"
             words.append(acc)
+        if self.xmin and self.gebf:
+            for w in range(S // 4):
+                e(f"{ind}const uint32_t hw{w} = {words[w]};")
+            words = [f"hw{w}" for w in range(S // 4)]
+        e(f"{ind}if (gidx >= a.b_lo) {{")
+        e(f"{ind}  const int gs = gidx - a.b_lo;")
+        e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {S // 16} * {NT};")
+        if self.EF:
+            e(f"{ind}  const uint64_t pol_h = gs < ef_lim ? pol_first : pol_last;")
+        if not (self.xmin and self.gebf):
+            for j in range(S):
+                if j not in pre:
+                    e(f"{ind}  const uint32_t h{j} = m{j} & {hm:#x}u;")
         for g in range(S // 16):
             ws = ", ".join(words[4 * g: 4 * g + 4])
             pol = "pol_h" if self.EF else "pol_last"
@@ -589,9 +608,13 @@ class Gen16:
             for j in range(S):
                 e(f"{ind}  m{j} = vt::mad_u32(h{j}, 0xFFFFFFFFu, m{j});")
         e(f"{ind}}}")
-        if self.xmin:  # r1/3: unconditional LOP3 clear, no phi moves (128.4 vs 127.3 Gbps)
+        if self.xmin:  # r1/3: unconditional clears after the branch (LOP3; IMAD for the CLRI states)
             for j in range(S):
-                e(f"{ind}m{j} &= {lm:#x}u;")
+                if j < self.clri:
+                    e(f"{ind}m{j} = vt::mad_u32(h{j}, 0xFFFFFFFFu, m{j});")
+                else:
+                    e(f"{ind}m{j} &= {lm:#x}u;")
+        e(f"{ind}}}")
         if tb_after:
             self.tb_step_both(ind, ge % 2)
         e(f"{ind}++gidx;")
@@ -627,7 +650,10 @@ class Gen16:
         e("  uint4* const s_llr = smem_dyn;")
         e(f"  uint4* const s_tb = smem_dyn + {4 * self.RS * NT};  // (even GPB only)")
         e("  (void)s_tb;")
-        e("  const uint64_t pol_last = vt::policy_evict_last();")
+        if self.polfrac:  # one fractional policy for every history store (no per-group select)
+            e(f"  const uint64_t pol_last = VT_POLICY_LAST_FIRST({self.polfrac});")
+        else:
+            e("  const uint64_t pol_last = vt::policy_evict_last();")
         if self.EF:
             e("  const uint64_t pol_first = vt::policy_evict_first();")
         if self.EF:

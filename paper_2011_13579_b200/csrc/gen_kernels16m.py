@@ -68,6 +68,8 @@ class Gen16M(Gen16):
         # ONE lane (min over its slots there + one shuffle from that lane) instead of the
         # per-lane tree over all 64 slots + 2 xor shuffles.  K=9 (753,561): T = {0, 193} /
         # {0, 4}, W_T = 9 / 10, Sb' = 2560: 2560 + 3328 + 3*512 = 7424 < 8192.
+        self.clri = int(os.environ.get("VT_CLRI16M", "32"))  # group end: IMAD clears (see group_end)
+        self.gebf = os.environ.get("VT_GEBF16M", "1") == "1"
         self.rsets = None
         self.GPB = self.P // self.L
         if not self.cheap and os.environ.get("VT_RSET", "1") == "1":
@@ -328,24 +330,41 @@ class Gen16M(Gen16):
         tb_after = bool(self.seed) and self.rng.random() < 0.5
         if not tb_after:
             self.tb_step(ind)
-        e(f"{ind}if (gidx >= a.b_lo) {{")
-        e(f"{ind}  const int gs = gidx - a.b_lo;")
-        e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {SQ} * {NT};")
-        for r in range(SL):
-            e(f"{ind}  const uint32_t h{r} = m{r} & {hm:#x}u;")
+        # fields of the first CLRI slots before the store branch, those slots cleared with
+        # IMADs (FMA pipe; the LOP3 clears load the ALU pipe); GEBF: fields and packs
+        # unconditional, only the stores under the branch (warm-up fields are zero)
+        pre = range(SL) if self.gebf else range(self.clri)
+        e(f"{ind}{{  // group-end scope (fields h, packs hw)")
+        for r in pre:
+            e(f"{ind}const uint32_t h{r} = m{r} & {hm:#x}u;")
         words = []
         for w in range(SL // 4):
             acc = f"h{4 * w}"
             for t in range(1, 4):
                 acc = f"vt::mad_u32(h{4 * w + t}, {1 << (L * t)}u, {acc})"
             words.append(acc)
+        if self.gebf:
+            for w in range(SL // 4):
+                e(f"{ind}const uint32_t hw{w} = {words[w]};")
+            words = [f"hw{w}" for w in range(SL // 4)]
+        e(f"{ind}if (gidx >= a.b_lo) {{")
+        e(f"{ind}  const int gs = gidx - a.b_lo;")
+        e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {SQ} * {NT};")
+        if not self.gebf:
+            for r in range(SL):
+                if r not in pre:
+                    e(f"{ind}  const uint32_t h{r} = m{r} & {hm:#x}u;")
         for g in range(SQ):
             ws = ", ".join(words[4 * g: 4 * g + 4])
             e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), pol_last);")
         e(f"{ind}}}")
         # clear unconditionally (warm-up groups carry no decision bits): no phi moves
         for r in range(SL):
-            e(f"{ind}m{r} &= {lm:#x}u;")
+            if r < self.clri:
+                e(f"{ind}m{r} = vt::mad_u32(h{r}, 0xFFFFFFFFu, m{r});")
+            else:
+                e(f"{ind}m{r} &= {lm:#x}u;")
+        e(f"{ind}}}")
         if tb_after:
             self.tb_step(ind)
         e(f"{ind}++gidx;")

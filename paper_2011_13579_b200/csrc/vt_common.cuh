@@ -92,6 +92,13 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// evict_last for the fraction FRAC of the accessed lines, evict_first for the rest
+#define VT_POLICY_LAST_FIRST(FRAC)                                                                      \
+  ([] {                                                                                                 \
+    uint64_t p;                                                                                         \
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, " #FRAC ";" : "=l"(p)); \
+    return p;                                                                                           \
+  }())
 // 16-byte global->shared copy; src_bytes = 0 zero-fills (out-of-range words).
 // (No .L2::cache_hint operand: ptxas 12.9 allocated its 64-bit policy descriptor to
 // an odd uniform register in the K=9 kernels, which traps as an illegal instruction.)
