@@ -303,6 +303,7 @@ def other_configs(torch, vt, dev, steps: int) -> list:
              ("K=9 r1/2 (753,561) V=54", 9, (0o753, 0o561), 1 << 28, 256, 54)]
     # the headline workload through the other kernel forms (VT_KERNEL_VARIANT)
     cases.append(("K=7 r1/2 F=256 tensor-core branch metrics (16x2tc)", 7, GENS, 1 << 28, 256, 42, "16x2tc"))
+    cases.append(("K=7 r1/2 F=256 mma.sync branch metrics (16x2mma)", 7, GENS, 1 << 28, 256, 42, "16x2mma"))
     cases.append(("K=7 r1/2 F=256 one window per thread (s32)", 7, GENS, 1 << 28, 256, 42, "s32"))
     for lw in (16, 18, 22):  # batch sweep at F=256 (2^20 windows is the headline)
         cases.append((f"K=7 r1/2 sweep windows=2^{lw} (F=256)", 7, GENS, 256 << lw, 256, 42))

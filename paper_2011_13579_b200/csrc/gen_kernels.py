@@ -424,6 +424,13 @@ def code_units(name: str, K: int, gens: tuple[int, ...]) -> list[tuple[str, str,
                            f"{gtc.S}, {gtc.CH}, {gtc.L}, {gtc.S // 16}, {gtc.P}, 0, {{{gl}}})"]))
         targ = ", const __grid_constant__ CUtensorMap tmap" if g16.tma else ""
         rows = g16.RS if g16.tma else 0  # TMA box lines per row (0: no tensor-map parameter)
+        if g16.cheap and g16.B == 2 and gen_kernels16.NT == 128:  # mma.sync branch metrics (VT_KERNEL_VARIANT=16x2mma)
+            gmx = Gen16(name, K, gens, mma=True)
+            units.append((f"vtk16mma_{name}.cu", gmx.kernel(),
+                          [f'extern "C" __global__ void vtk16mma_{name}(const vt::StreamArgs a{targ});',
+                           f'extern "C" __global__ void vtk16mmanf_{name}(const vt::StreamArgs a{targ});'],
+                          [f"VT_KERNEL(vtk16mma_{name}, &vtk16mmanf_{name}, {gmx.SMEM}, 2, 128, {K}, {len(gens)}, 1, 2, "
+                           f"{gmx.S}, {gmx.CH}, {gmx.L}, {gmx.S // 16}, {gmx.P}, {rows}, {{{gl}}})"]))
         units.append((f"vtk16_{name}.cu", g16.kernel(),
                       [f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a{targ});',
                        f'extern "C" __global__ void vtk16nf_{name}(const vt::StreamArgs a{targ});'],

@@ -133,7 +133,7 @@ def renorm_set(K: int, gens: tuple[int, ...], wmax: int, allowed=None, max_size:
 
 
 class Gen16:
-    def __init__(self, name: str, K: int, gens: tuple[int, ...], tc: bool = False):
+    def __init__(self, name: str, K: int, gens: tuple[int, ...], tc: bool = False, mma: bool = False):
         self.name = name
         self.K = K
         self.k = K - 1
@@ -248,6 +248,16 @@ class Gen16:
             self.SMEM += 16 * (NT // 32)
         # tensor-core branch metrics (paper formulation): int8 LLR tile x +-8 codeword matrix
         self.tc = tc
+        # mma.sync register-fragment branch metrics (the 16x2mma form, see mma_block): per body and
+        # warp, 12 mma.sync.m16n8k16 s8 of the realigned LLR words against the +-8 codeword matrix;
+        # A fragments through a transposed shared-memory tile, D fragments back to the owning
+        # threads with stmatrix; per warp 8 x 33 + 32 x 32 words of shared memory
+        self.mma = mma
+        if mma:
+            assert self.cheap and self.B == 2 and self.pbr and NT == 128 and self.P == 6
+            self.MXOFF = self.SMEM
+            self.MXW = (8 * 33 + 32 * 32) * 4
+            self.SMEM += self.MXW * (NT // 32)
         # tc: rows-ready mbarrier instead of a CTA-wide __syncthreads before each MMA issue
         self.tc_mbar = tc and os.environ.get("VT_TC_SYNC", "mbar") == "mbar"
         if tc:
@@ -274,6 +284,10 @@ class Gen16:
         in TMEM (one 32x32b.x4 load per window set: the 4 pattern columns of the stage)."""
         e = self.emit
         pats = sorted(set(pats))
+        if self.mma:
+            if q % 2 == 0:
+                self.mma_block(ind, q // 2)
+            return
         if not self.tc:
             for p in pats:
                 expr = " + ".join(f"{'N' if (p >> b) & 1 else 'U'}{q}_{b}" for b in range(self.B))
@@ -288,6 +302,83 @@ class Gen16:
             e(f"{ind}const uint32_t S{q}_{p} = vt::prmt(ta{q}_{p}, tb{q}_{p}, 0x5410u);")
         if q + 1 < self.P:
             self.tc_load(ind, q + 1)
+
+    def mma_block(self, ind: str, sp: int) -> None:
+        """Pattern sums of body stages 2sp, 2sp+1 on the tensor cores (mma.sync, SURVEY.md:270-273).
+        Tile m (m = 0..3) of the warp's 64 windows: row g = window A and row g+8 = window B of
+        lane 4g+m; D[row][n] = 2048 + sum_k llr[row][k] * W[k][n] = S_p of stage 2sp + n/4,
+        p = n%4 (W = +-8 codeword entries: the kernel's U/N scaling, module docstring).  Lane
+        (g,q) gets columns 2q, 2q+1 of its quad's rows; PRMT packs windows A/B into 16x2 words
+        (X: even columns, Y: odd) and stmatrix writes them as rows of the owning lanes' tiles, so
+        after a __syncwarp each lane reads its 8 words with two 16-byte loads."""
+        e = self.emit
+        e(f"{ind}uint32_t mX{sp}[4], mY{sp}[4];")
+        e(f"{ind}#pragma unroll")
+        e(f"{ind}for (int m = 0; m < 4; ++m) {{")
+        e(f"{ind}  uint32_t d0, d1, d2, d3;")
+        e(f"{ind}  vt::mx::mma_s8_16816(d0, d1, d2, d3, ma0[m], ma1[m], mb{sp}, 2048u);")
+        e(f"{ind}  mX{sp}[m] = vt::prmt(d0, d2, 0x5410u);")
+        e(f"{ind}  mY{sp}[m] = vt::prmt(d1, d3, 0x5410u);")
+        e(f"{ind}}}")
+        e(f"{ind}vt::mx::stmatrix_x4(mst0 + mstc({sp}, 0), mX{sp}[0], mY{sp}[0], mX{sp}[1], mY{sp}[1]);")
+        e(f"{ind}vt::mx::stmatrix_x4(mst1 + mstc({sp}, 1), mX{sp}[2], mY{sp}[2], mX{sp}[3], mY{sp}[3]);")
+        e(f"{ind}__syncwarp();")
+        e(f"{ind}const uint4 mvx{sp} = *reinterpret_cast<const uint4*>(ys + mrd({2 * sp}));")
+        e(f"{ind}const uint4 mvy{sp} = *reinterpret_cast<const uint4*>(ys + mrd({2 * sp + 1}));")
+        q0, q1 = 2 * sp, 2 * sp + 1
+        for nm, v in ((f"S{q0}_0", f"mvx{sp}.x"), (f"S{q0}_2", f"mvx{sp}.y"), (f"S{q1}_0", f"mvx{sp}.z"),
+                      (f"S{q1}_2", f"mvx{sp}.w"), (f"S{q0}_1", f"mvy{sp}.x"), (f"S{q0}_3", f"mvy{sp}.y"),
+                      (f"S{q1}_1", f"mvy{sp}.z"), (f"S{q1}_3", f"mvy{sp}.w")):
+            e(f"{ind}const uint32_t {nm} = {v};")
+
+    def mma_setup(self) -> None:
+        """Per-lane constants of the 16x2mma form: B fragments (codeword matrix of each stage
+        pair), stmatrix row addresses, the lane's own tile row; rows 3 and 7 of the transposed
+        A tile are zero (bytes 12..15 of a body)."""
+        e = self.emit
+        e(f"  char* const s_mxw = reinterpret_cast<char*>(smem_dyn) + {self.MXOFF} + (tid >> 5) * {self.MXW};")
+        e("  uint32_t* const xsT = reinterpret_cast<uint32_t*>(s_mxw);  // [8 words][33 lanes]: the body's LLR words")
+        e("  char* const ys = s_mxw + 1056;  // [32 lanes][8 x 16 B]: the lanes' pattern sums")
+        e("  const int mlane = tid & 31, mg = mlane >> 2, mq = mlane & 3;")
+        e("  xsT[3 * 33 + mlane] = 0u;")
+        e("  xsT[7 * 33 + mlane] = 0u;")
+        e("  // B fragment of stage pair sp: rows k = 4q..4q+3 of column n = g (stage 2sp + n/4, pattern n%4):")
+        e("  // +8 / -8 where byte k is LLR b of that stage and bit b of the pattern is 0 / 1")
+        for sp in range(3):
+            e(f"  uint32_t mb{sp} = 0u;")
+            e("  #pragma unroll")
+            e("  for (int i = 0; i < 4; ++i) {")
+            e(f"    const int k = 4 * mq + i, st = {2 * sp} + (mg >> 2), p = mg & 3;")
+            e("    const int v = ((k >> 1) == st) ? ((((p >> (k & 1)) & 1) != 0) ? -8 : 8) : 0;")
+            e(f"    mb{sp} |= (uint32_t)(v & 0xFF) << (8 * i);")
+            e("  }")
+        e("  // tile rows: lane L's row at ys + 128 L, chunk c at ((c + f(L)) & 7) * 16 with")
+        e("  // f(L) = 4 ((L >> 2) & 1) + (((L & 3) + (L >> 3)) & 3): conflict-free for the stmatrix")
+        e("  // rows (lanes 4r + m) and for the owners' 16-byte loads (8 consecutive lanes)")
+        e("  auto mf = [](int L) { return 4 * ((L >> 2) & 1) + (((L & 3) + (L >> 3)) & 3); };")
+        e("  const int mfo = mf(mlane);")
+        e("  auto mrd = [&](int c) { return mlane * 128 + (((c + mfo) & 7) << 4); };")
+        e("  // stmatrix: lanes 8j + r address row r of matrix j = (X, Y) of tiles 2h + (j >> 1): owner 4r + 2h + (j >> 1)")
+        e("  const int mL0 = 4 * (mlane & 7) + (mlane >> 4), mL1 = mL0 + 2;")
+        e("  const uint32_t mst0 = vt::tc::smem_u32(ys) + mL0 * 128, mst1 = vt::tc::smem_u32(ys) + mL1 * 128;")
+        e("  const int mf0 = mf(mL0) + ((mlane >> 3) & 1), mf1 = mf(mL1) + ((mlane >> 3) & 1);")
+        e("  auto mstc = [&](int sp, int h) { return (uint32_t)((((2 * sp) + (h ? mf1 : mf0)) & 7) << 4); };")
+        e("  uint32_t ma0[4], ma1[4];  // A fragments of the body (tiles m = 0..3)")
+
+    def mma_body_a(self, ind: str) -> None:
+        """A fragments of this body: every lane stores its realigned words into the transposed
+        tile, then lane (g,q) loads word q of windows A/B of lanes 4g+m (m = 0..3)."""
+        e = self.emit
+        e(f"{ind}__syncwarp();  // the previous body's A-fragment loads are done")
+        for k in range(3):
+            e(f"{ind}xsT[{k} * 33 + mlane] = curA[{k}];")
+            e(f"{ind}xsT[{4 + k} * 33 + mlane] = curB[{k}];")
+        e(f"{ind}__syncwarp();")
+        e(f"{ind}#pragma unroll")
+        e(f"{ind}for (int m = 0; m < 4; ++m) {{")
+        e(f"{ind}  ma0[m] = xsT[mq * 33 + 4 * mg + m];")
+        e(f"{ind}  ma1[m] = xsT[(4 + mq) * 33 + 4 * mg + m];")
+        e(f"{ind}}}")
 
     def tc_load(self, ind: str, q: int) -> None:
         e = self.emit
@@ -309,7 +400,7 @@ class Gen16:
         gq = q % L
         flag = f"cflag{q - gq}"
         e = self.emit
-        for b in range(B if not self.tc else 0):
+        for b in range(B if not (self.tc or self.mma) else 0):
             byte = q * B + b
             w, k = byte >> 2, byte & 3
             sel = k | ((8 | k) << 4) | ((4 + k) << 8) | ((12 + k) << 12)
@@ -629,7 +720,7 @@ class Gen16:
           f"two windows per thread (16x2 halves), {self.L}-bit history groups, {self.P}-stage body, {self.CH}-stage chunks")
         e('#include "../vt_common.cuh"')
         e("")
-        pre = "vtk16tc" if self.tc else "vtk16"
+        pre = "vtk16tc" if self.tc else ("vtk16mma" if self.mma else "vtk16")
         for fm in (True, False):
             self.fm = fm
             self.kernel_one(f"{pre}_{self.name}" if fm else f"{pre}nf_{self.name}")
@@ -650,6 +741,8 @@ class Gen16:
         e("  uint4* const s_llr = smem_dyn;")
         e(f"  uint4* const s_tb = smem_dyn + {4 * self.RS * NT};  // (even GPB only)")
         e("  (void)s_tb;")
+        if self.mma:
+            self.mma_setup()
         if self.polfrac:  # one fractional policy for every history store (no per-group select)
             e(f"  const uint64_t pol_last = VT_POLICY_LAST_FIRST({self.polfrac});")
         else:
@@ -794,7 +887,7 @@ class Gen16:
         elif not self.tc:
             e("    uint32_t curA[NWC], curB[NWC];")
         e("    // leading zero-LLR padding keeps all-zero metrics at zero: skip whole bodies of it")
-        if self.tc:  # warp-uniform: tcgen05.ld is .sync.aligned, so every lane must run the same bodies
+        if self.tc or self.mma:  # warp-uniform: tcgen05.ld / mma.sync / stmatrix are .sync.aligned, so every lane must run the same bodies
             e(f"    const int it0 = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)min(min(max(gA.s - gA.g0, (int64_t)0), "
               f"max(gB.s - gB.g0, (int64_t)0)) / {P}, (int64_t){self.CHB}));")
         else:
@@ -878,6 +971,8 @@ class Gen16:
             for w in ("A", "B"):
                 e(f"        vt::realign_row_at<{self.NWB}>(cur{w}, llr{w}(c & 1), ((mo{w} + CH * B * c) & 15) + {P * B} * it, "
                   f"min(max((pad{w} - CH * c - {P} * it) * B, 0), {P * B}));")
+            if self.mma:
+                self.mma_body_a("        ")
         names = [f"m{j}" for j in range(S)]
         deferred: list = []
         for q in range(P):

@@ -89,6 +89,7 @@ class Gen16M(Gen16):
         assert self.Sb + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)), "metric range"
         self.pbr = True
         self.tc = False
+        self.mma = False
         self.CHB = int(os.environ.get("VT_CHB16M", "5"))  # 5-body chunks: one traceback settle per chunk (see Gen16)
         self.CH = self.P * self.CHB
         self.NWB = -(-self.P * self.B // 4)

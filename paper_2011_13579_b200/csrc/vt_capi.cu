@@ -77,7 +77,7 @@ struct KernelEntry {
   const void* fn;
   const void* fn_nofm;  // variant without final-metric bookkeeping (nullptr: use fn)
   int smem;             // dynamic shared memory bytes per CTA
-  int tc;               // 1: tensor-core branch-metric variant (opt-in)
+  int tc;               // 1: tcgen05 / 2: mma.sync branch-metric variant (opt-in)
   int nt;               // threads per CTA
   // kernels of a runtime-loaded code module (vt_load_code_module) launch through the module,
   // which carries its own CUDA runtime registration of them
@@ -110,13 +110,15 @@ std::mutex g_dyn_mu;
 // Kernel variant: "16x2" (two windows per thread -- per group of 2/4 lanes for K=8/9 --
 // in packed 16-bit halves), "s32" (one window per thread, 32-bit metrics) or "16x2tc"
 // (16x2 with the branch metrics of each 12-stage chunk computed on the tensor cores:
-// tcgen05 kind::i8, the paper's LLR x codeword-matrix contraction).  Default: 16x2
+// tcgen05 kind::i8, the paper's LLR x codeword-matrix contraction) or "16x2mma" (the same
+// contraction per body with mma.sync.m16n8k16 s8 register fragments; tc = 2).  Default: 16x2
 // where it exists with 3-bit history groups (measured fastest for every such code);
 // s32 otherwise.  VT_KERNEL_VARIANT forces one.
 int variant_rank(const KernelEntry* e, const char* env) {
   // lower is better; entries of the requested variant win, then the default order
   const bool is16 = e->WPT > 1, istc = e->tc != 0;
-  if (env && strcmp(env, "16x2tc") == 0) return istc ? 0 : (is16 ? 1 : 2);
+  if (env && strcmp(env, "16x2tc") == 0) return e->tc == 1 ? 0 : (is16 && !istc ? 1 : 2);
+  if (env && strcmp(env, "16x2mma") == 0) return e->tc == 2 ? 0 : (is16 && !istc ? 1 : 2);
   if (env && strcmp(env, "16x2") == 0) return (is16 && !istc) ? 0 : (istc ? 2 : 1);
   if (env && strcmp(env, "s32") == 0) return is16 ? 2 : 0;
   if (istc) return 3;                       // opt-in only
@@ -194,7 +196,7 @@ int prepare(const KernelEntry* k) {
             k->tc, occ, (int)e, fa.numRegs, fa.sharedSizeBytes, k->smem, fa.maxDynamicSharedSizeBytes);
   }
   if (e != cudaSuccess || occ < 1) occ = 1;
-  if (k->tc && e == cudaSuccess) {
+  if (k->tc == 1 && e == cudaSuccess) {
     // The occupancy query answers 1 for the tcgen05 kernels although two CTAs fit (256 TMEM
     // columns each, 2 x ~77 KB shared memory, <= 240 registers): size by those limits.
     cudaFuncAttributes fa;

@@ -522,4 +522,23 @@ __device__ __forceinline__ void dealloc(uint32_t taddr) {  // one full warp
 }
 }  // namespace tc
 
+// --- mma.sync register-fragment branch metrics (the 16x2mma form, gen_kernels16.py) ---
+namespace mx {
+// D = A (16x16 s8, row) . B (16x8 s8, col) + C (s32): a0 rows g, a1 rows g+8 (bytes 4q..4q+3),
+// b0 rows 4q..4q+3 of column g, d0/d1 row g cols 2q/2q+1, d2/d3 row g+8 (g = lane/4, q = lane%4)
+__device__ __forceinline__ void mma_s8_16816(uint32_t& d0, uint32_t& d1, uint32_t& d2, uint32_t& d3, uint32_t a0,
+                                             uint32_t a1, uint32_t b0, uint32_t c) {
+  asm("mma.sync.aligned.m16n8k16.row.col.s32.s8.s8.s32 {%0, %1, %2, %3}, {%4, %5}, {%6}, {%7, %7, %7, %7};"
+      : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3)
+      : "r"(a0), "r"(a1), "r"(b0), "r"(c));
+}
+// four 8x8 b16 matrices: lane t holds row t/4, columns 2(t%4), 2(t%4)+1 of matrix i in r_i; lanes
+// 8i..8i+7 give the shared addresses of matrix i's rows
+__device__ __forceinline__ void stmatrix_x4(uint32_t saddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(r0), "r"(r1),
+               "r"(r2), "r"(r3)
+               : "memory");
+}
+}  // namespace mx
+
 }  // namespace vt

@@ -38,7 +38,7 @@ def _llr(n, kind, seed):
     return q
 
 
-@pytest.mark.parametrize("variant", ["16x2", "s32", "16x2tc"])
+@pytest.mark.parametrize("variant", ["16x2", "s32", "16x2tc", "16x2mma"])
 @pytest.mark.parametrize("case", _cases(), ids=lambda c: f"n{c[0]}-F{c[1]}-V{c[2]}-{c[3]}")
 def test_fuzz_stream(case, variant, monkeypatch):
     import torch
@@ -53,7 +53,7 @@ def test_fuzz_stream(case, variant, monkeypatch):
     np.testing.assert_array_equal(got, want)
 
 
-@pytest.mark.parametrize("variant", ["16x2", "16x2tc"])
+@pytest.mark.parametrize("variant", ["16x2", "16x2tc", "16x2mma"])
 @pytest.mark.parametrize("case", _cases(seed=7, count=6), ids=lambda c: f"n{c[0]}-F{c[1]}-V{c[2]}-{c[3]}")
 def test_fuzz_window_ranges(case, variant, monkeypatch, tmp_path):
     """Window-range launches on stage sub-buffers (the streaming/sharding path)."""

@@ -13,7 +13,8 @@ pytestmark = pytest.mark.gpu
 # (K, generators, windows per CTA of the form, VT_KERNEL_VARIANT)
 FORMS = [(7, (0o171, 0o133), 256, None), (7, (0o133, 0o171, 0o165), 256, None), (9, (0o753, 0o561), 64, None),
          (8, (0o247, 0o371), 64, None), (7, (0o171, 0o133), 128, "s32"), (9, (0o753, 0o561), 32, "s32"),
-         (7, (0o171, 0o133), 256, "16x2tc"), (5, (0o23, 0o35), 128, None), (8, (0o247, 0o371), 64, "s32")]
+         (7, (0o171, 0o133), 256, "16x2tc"), (5, (0o23, 0o35), 128, None), (8, (0o247, 0o371), 64, "s32"),
+         (7, (0o171, 0o133), 256, "16x2mma")]
 
 
 @pytest.mark.parametrize("fl", [400, 1024])

@@ -157,7 +157,7 @@ def test_final_metrics_match_oracle(vt):
     np.testing.assert_array_equal(metric, want_metric.astype(np.float64))
 
 
-@pytest.mark.parametrize("variant", ["16x2", "s32", "16x2tc"])
+@pytest.mark.parametrize("variant", ["16x2", "s32", "16x2tc", "16x2mma"])
 @pytest.mark.parametrize("code", ["k7r2", "k7r3", "k8r2", "k9r2"])
 @pytest.mark.parametrize("fv", [(256, 42), (100, 20), (37, 5)])
 def test_kernel_variants_match_oracle(vt, code, fv, variant, monkeypatch):

@@ -174,7 +174,7 @@ def test_adversarial_gap_stream_decodes_exactly(name, fv):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", ["16x2", "s32"])
+@pytest.mark.parametrize("variant", ["16x2", "s32", "16x2mma"])
 @pytest.mark.parametrize("name", sorted(CODES))
 @pytest.mark.parametrize("fv", [(256, 42), (1000, 60), (31, 7), (24000, 0)])
 def test_adversarial_stream_decodes_exactly(name, fv, variant, monkeypatch):
