@@ -72,8 +72,9 @@ class Gen16M(Gen16):
         self.gebf = os.environ.get("VT_GEBF16M", "1") == "1"
         self.rsets = None
         self.GPB = self.P // self.L
-        if not self.cheap and os.environ.get("VT_RSET", "1") == "1":
-            wmax = ((1 << (16 - self.L)) - 1 - delta - self.L * 2 * self.dmax) // 256
+        if os.environ.get("VT_RSET", "1") == "1":
+            # (the cheap middle stage needs metrics >= 2*dmax at its input: Sb' = 256 W_T + 2*dmax)
+            wmax = ((1 << (16 - self.L)) - 1 - delta - self.L * 2 * self.dmax - self.Sb) // 256
             found = []
             for ge in range(self.GPB):
                 lo = self.top - self.L * (ge + 1)
@@ -85,7 +86,7 @@ class Gen16M(Gen16):
                 found.append(best)
             if all(f is not None for f in found):
                 self.rsets = found
-                self.Sb = 256 * max(f[1] for f in found)
+                self.Sb += 256 * max(f[1] for f in found)
         assert self.Sb + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)), "metric range"
         self.pbr = True
         self.tc = False
