@@ -72,6 +72,13 @@ class ClockSampler:
         for ln in self.proc.stdout:
             self.lines.append(ln.strip())
 
+    def mark_start(self):
+        self.i0 = len(self.lines)
+
+    def mark_end(self):
+        time.sleep(0.15)  # the sample taken across the region's end
+        self.i1 = len(self.lines)
+
     def __exit__(self, *exc):
         if self.proc is not None:
             self.proc.terminate()
@@ -83,7 +90,11 @@ class ClockSampler:
     def summary(self) -> dict:
         sm, mx, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        # the samples around the timed region: from the last one before it (a short region may
+        # hold none of the 100 ms samples) to the first one after it
+        i0 = max(0, getattr(self, "i0", 1) - 1)
+        i1 = getattr(self, "i1", len(self.lines))
+        for ln in self.lines[i0:i1]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -184,20 +195,24 @@ def run_ours(args) -> None:
     def step():
         vt.decode_stream_device(q, spec, F, V, out=out, stream=stream)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    # the clock sampler starts first (it waits 0.3 s for nvidia-smi): the warm-up steps then
+    # run right before the timed ones, so the timed region does not start from idle clocks
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk.mark_start()
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
     if ws > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)

@@ -10,7 +10,7 @@ import paper_2011_13579_b200 as vt
 from oracle import oracle
 FORMS = [(7, (0o171, 0o133), None), (7, (0o133, 0o171, 0o165), None), (9, (0o753, 0o561), None),
          (8, (0o247, 0o371), None), (7, (0o171, 0o133), "s32"), (7, (0o171, 0o133), "16x2tc"), (5, (0o23, 0o35), None),
-         (9, (0o753, 0o561), "s32")]
+         (9, (0o753, 0o561), "s32"), (7, (0o171, 0o133), "16x2mma"), (9, (0o561, 0o753), None)]
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 t_end = time.time() + float(sys.argv[2] if len(sys.argv) > 2 else 300)
 fails = 0; runs = 0
