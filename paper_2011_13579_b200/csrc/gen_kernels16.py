@@ -19,8 +19,9 @@ Per 16-bit half:  U = Lambda * 2^L + h  (unsigned), where
     (both >= 0), so each stage adds delta + 128*B >= 0; at each group start the
     metrics are renormalised by Lambda_0 - S_b (S_b bounds the metric spread),
     keeping Lambda in [0, 2*S_b + L*256*B] < 2^(16-L) (L = 3 for K=7 r1/2); K=7
-    r1/3 renormalises by the exact per-half minimum instead (Gen16.xmin), which
-    halves the span and also fits L = 3.  Per-half arithmetic is modular; the
+    r1/3 renormalises by a per-half minimum instead (Gen16.xmin: over a small
+    state set T, renorm_set, within 256 * W_T of the exact minimum), which
+    shrinks the span and also fits L = 3.  Per-half arithmetic is modular; the
     true values stay in range, so the unsigned max is exact.
 At each group end the L-bit fields are masked out, packed 4 states per word
 (12 bits per half), streamed to the scratch slot and cleared.  The traceback

@@ -13,9 +13,11 @@ lane -- the register budget of the K=7 kernel.
   3-bit history groups for K=9) run lane-locally before a shared-memory
   transpose returns it to the top bits.  The lane-dependent part of each branch
   pattern is a per-lane swap of the U/N terms (LOP3 select with a lane mask).
-* Renormalisation by the exact per-half minimum over all states (per-lane
-  VIMNMX3 tree + 2 shuffles): the metric spread of (753,561) is bounded by
-  Delta = 256 x 13, so Lambda in [Sb', Sb' + Delta + 3*512) fits 13 bits.
+* Renormalisation by the per-half minimum over a small state set T living on
+  one lane (gen_kernels16.renorm_set; one shuffle from that lane; round 1: the
+  exact minimum, a per-lane VIMNMX3 tree + 2 shuffles): the metric spread of
+  (753,561) is bounded by Delta = 256 x 13 and min_T is within 256 * W_T of the
+  exact minimum, so Lambda in [0, Sb' + Delta + 3*512) fits 13 bits.
 * Shared memory per CTA: LLR rows per window pair (each lane stages every T-th
   16-byte chunk; rows are read by all T lanes), the per-thread traceback ring
   (cp.async prefetch of whole history groups, 4 deep) and the transpose buffer.

@@ -123,7 +123,8 @@ int variant_rank(const KernelEntry* e, const char* env) {
   if (env && strcmp(env, "s32") == 0) return is16 ? 2 : 0;
   if (istc) return 3;                       // opt-in only
   // 16x2 preferred wherever 3-bit history groups fit (K=7 r1/2: 163 vs 118 Gbps; K=7 r1/3
-  // with exact-minimum renormalisation: 127.5 vs 113; K=9 over 4 lanes: 32.3 vs 25.1)
+  // with exact-minimum renormalisation: 127.5 vs 113 -- 143.4 with the subset minimum; K=9 over
+  // 4 lanes: 32.3 vs 25.1 -- 36.8 with the subset minimum)
   if (is16) return e->BL >= 3 ? 0 : 2;
   return 1;
 }

@@ -70,7 +70,7 @@ def test_fuzz_window_ranges(case, variant, monkeypatch, tmp_path):
 
 
 # K=8 / K=9: the multi-lane 16x2 kernels (states over 2 / 4 lanes, shared-memory transpose,
-# exact-minimum renormalisation) and the s32 kernels
+# subset-minimum renormalisation) and the s32 kernels
 _CODES89 = {"k9r2": (9, (0o753, 0o561)), "k8r2": (8, (0o247, 0o371))}
 
 
