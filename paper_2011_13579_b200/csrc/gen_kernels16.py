@@ -41,10 +41,11 @@ CH_BODIES = 2  # loop bodies per LLR chunk
 MINB16 = 1  # CTAs per SM bound (3 forces a 168-register cap: spills, measured 16% slower with the ring traceback)
 
 
-# Emission seeds picked by measurement (tools/_gpu_var.sh over VT_SEED16 / VT_SEED16M = 0..7,
-# 2^28 stages, profiles/r2_schedule_sweep.txt): K=7 r1/3 seed 5 130.7 vs 129.3 Gbps,
-# K=9 seed 7 33.52 vs 33.37; K=7 r1/2 keeps the default order (the fastest of 13).
-MEASURED_SEEDS = {(7, (0o133, 0o171, 0o165)): 5, (9, (0o753, 0o561)): 7}
+# Emission seeds picked by measurement (tools/_gpu_var.sh / _gpu_ab2.sh over VT_SEED16 / VT_SEED16M =
+# 0..7, 2^28 stages, profiles/r2_schedule_sweep.txt, r2_seed_ab.txt).  Re-swept after the subset
+# minimum (round 2b): K=7 r1/3 seed 0 143.65 (seeds 1-7: 141.9-143.5), K=9 seed 5 36.90 (35.9-36.8);
+# K=7 r1/2 keeps the default order (the fastest of 13).
+MEASURED_SEEDS = {(9, (0o753, 0o561)): 5}
 
 
 def history_bits(K: int, B: int) -> int:
