@@ -230,6 +230,7 @@ class Gen16:
                        and 4 * ((-(-(15 + self.P * int(os.environ.get("VT_CHB16", "5")) * self.B + 4) // 16)) | 1)
                        >= 4 * (self.S // 16) and "VT_TBD16" not in os.environ)
         self.EF = int(os.environ.get("VT_EF16", "64" if self.cheap_candidate() else "0"))  # 1/256 of the stored groups
+        self.efc = os.environ.get("VT_EFC16", "0") == "1"  # evict-first split per chunk instead of per group
         self.polfrac = os.environ.get("VT_POLFRAC16", "")  # e.g. "0.75": fractional evict_last/evict_first
         if self.polfrac:
             self.EF = 0
@@ -688,14 +689,15 @@ class Gen16:
         e(f"{ind}  const int gs = gidx - a.b_lo;")
         e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {S // 16} * {NT};")
         if self.EF:
-            e(f"{ind}  const uint64_t pol_h = gs < ef_lim ? pol_first : pol_last;")
+            if not self.efc:
+                e(f"{ind}  const uint64_t pol_h = gs < ef_lim ? pol_first : pol_last;")
         if not (self.xmin and self.gebf):
             for j in range(S):
                 if j not in pre:
                     e(f"{ind}  const uint32_t h{j} = m{j} & {hm:#x}u;")
         for g in range(S // 16):
             ws = ", ".join(words[4 * g: 4 * g + 4])
-            pol = "pol_h" if self.EF else "pol_last"
+            pol = ("pol_c" if self.efc else "pol_h") if self.EF else "pol_last"
             e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), {pol});")
         if not self.xmin:  # IMAD clear (FMA pipe): the ALU pipe is the K=7 r1/2 bottleneck
             for j in range(S):
@@ -950,6 +952,9 @@ class Gen16:
         e(f"    int gidx = it0 * {self.GPB};")
         e("    // traceback of the previous tile: one group step per forward group, loads one group ahead")
         e("    for (int c = 0; c < a.nc; ++c) {")
+        if self.EF and self.efc:
+            e(f"      // history L2 policy per chunk (CTA-uniform: no per-store uniform-register move)")
+            e(f"      const uint64_t pol_c = (c * {self.CHB * self.GPB} - a.b_lo < ef_lim) ? pol_first : pol_last;")
         if self.tc:
             e("      const int64_t onA = oA + (int64_t)CH * B * (c + 1), onB = oB + (int64_t)CH * B * (c + 1);")
         if self.tc:
