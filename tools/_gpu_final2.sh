@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/f2_pytest_all.log 2>&1; echo "rc $?" >> gpurun_out/f2_pytest_all.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f2_smoke.log 2>&1; echo "rc $?" >> gpurun_out/f2_smoke.log
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/f2_bench.json 2>gpurun_out/f2_bench.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/f2_bench_ref.json 2>gpurun_out/f2_bench_ref.err
+timeout 1800 bash tools/profile_round.sh r2c > gpurun_out/f2_profile_round.log 2>&1
