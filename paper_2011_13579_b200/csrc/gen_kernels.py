@@ -434,7 +434,7 @@ def code_units(name: str, K: int, gens: tuple[int, ...]) -> list[tuple[str, str,
         units.append((f"vtk16_{name}.cu", g16.kernel(),
                       [f'extern "C" __global__ void vtk16_{name}(const vt::StreamArgs a{targ});',
                        f'extern "C" __global__ void vtk16nf_{name}(const vt::StreamArgs a{targ});'],
-                      [f"VT_KERNEL(vtk16_{name}, &vtk16nf_{name}, {g16.SMEM}, 0, {gen_kernels16.NT}, {K}, {len(gens)}, "
+                      [f"VT_KERNEL(vtk16_{name}, &vtk16nf_{name}, {g16.SMEM}, {3 if g16.tmh else 0}, {gen_kernels16.NT}, {K}, {len(gens)}, "
                        f"1, 2, {g16.S}, {g16.CH}, {g16.L}, {g16.S // 16}, {g16.P}, {rows}, {{{gl}}})"]))
     return units
 

@@ -231,6 +231,12 @@ class Gen16:
                        >= 4 * (self.S // 16) and "VT_TBD16" not in os.environ)
         self.EF = int(os.environ.get("VT_EF16", "64" if self.cheap_candidate() else "0"))  # 1/256 of the stored groups
         self.efc = os.environ.get("VT_EFC16", "0") == "1"  # evict-first split per chunk instead of per group
+        # TMEM history window (see tmh_* below): 16 of a tile's stored-group positions live in the
+        # CTA's tensor memory (256 columns x 128 lanes: one 16-word group per thread and column
+        # block) instead of the HBM scratch slot
+        self.tmh = (os.environ.get("VT_TMH16", "0") == "1" and not tc and not mma and self.pbr and NT == 128
+                    and self.S == 64)
+
         self.polfrac = os.environ.get("VT_POLFRAC16", "")  # e.g. "0.75": fractional evict_last/evict_first
         if self.polfrac:
             self.EF = 0
@@ -249,6 +255,10 @@ class Gen16:
         if self.tma:  # the TMA barriers after the rows (keeps the rows' alignment)
             self.SMEM_TMA_OFF = self.SMEM
             self.SMEM += 16 * (NT // 32)
+        if self.tmh:
+            self.SMEM_TM_OFF = self.SMEM  # TMEM allocation result
+            self.SMEM += 16
+
         # tensor-core branch metrics (paper formulation): int8 LLR tile x +-8 codeword matrix
         self.tc = tc
         # mma.sync register-fragment branch metrics (the 16x2mma form, see mma_block): per body and
@@ -531,12 +541,39 @@ class Gen16:
         S, SQ = self.S, self.S // 16
         e = self.emit
         e(f"{ind}{{")
-        e(f"{ind}  const uint32_t xo = (uint32_t)(txa + txs * max({grp}, a.b_lo)) * {SQ * NT * 16}u;")
-        e(f"{ind}  uint4* const dst = s_tb + ({ring}) * {SQ * NT} + tid;")
-        for q in range(SQ):
-            e(f"{ind}  vt::cp_async16(dst + {q * NT}, slotc + xo + {q * NT * 16}u, 16, 0);")
+        self.fetch_group(ind + "  ", grp, f"s_tb + ({ring}) * {SQ * NT} + tid")
         e(f"{ind}  vt::cp_async_commit();")
         e(f"{ind}}}")
+
+    def fetch_group(self, ind: str, grp: str, dst_expr: str) -> None:
+        """Group `grp` (clamped to a stored group) of the traced tile into the per-thread ring
+        entry at `dst`: cp.async from the HBM scratch slot, or (tmh) from the TMEM window --
+        tcgen05.ld of the thread's 16 words + shared-memory stores (warp-uniform choice)."""
+        SQ = self.S // 16
+        e = self.emit
+        dst = "dst"
+        if self.tmh:
+            e(f"{ind}uint4* const dst = {dst_expr};")
+            e(f"{ind}const int tpos = txa + txs * max({grp}, a.b_lo);")
+            e(f"{ind}if (tmw_tb && (unsigned)(tpos - tm_p0) < 16u) {{")
+            e(f"{ind}  uint32_t v[16];")
+            e(f"{ind}  vt::tc::ld16(tm_lane + (uint32_t)(tpos - tm_p0) * 16u, v);")
+            e(f"{ind}  vt::tc::wait_ld();")
+            for q in range(SQ):
+                e(f"{ind}  {dst}[{q * NT}] = make_uint4(v[{4 * q}], v[{4 * q + 1}], v[{4 * q + 2}], v[{4 * q + 3}]);")
+            e(f"{ind}}} else {{")
+            ii = ind + "  "
+        else:
+            ii = ind
+        if self.tmh:
+            e(f"{ii}const uint32_t xo = (uint32_t)tpos * {SQ * NT * 16}u;")
+        else:
+            e(f"{ii}const uint32_t xo = (uint32_t)(txa + txs * max({grp}, a.b_lo)) * {SQ * NT * 16}u;")
+            e(f"{ii}uint4* const dst = {dst_expr};")
+        for q in range(SQ):
+            e(f"{ii}vt::cp_async16({dst} + {q * NT}, slotc + xo + {q * NT * 16}u, 16, 0);")
+        if self.tmh:
+            e(f"{ind}}}")
 
     def drain_entry(self, r: str) -> str:
         """Ring entry r (0..7) of the last-tile drain: 0-3 the traceback ring, 4-7 the LLR row
@@ -553,10 +590,7 @@ class Gen16:
         e = self.emit
         e(f"{ind}__syncthreads();  // every warp is done with its LLR rows (entries 4-7 span all threads' rows)")
         e(f"{ind}for (int r = 4; r < 8; ++r) {{  // groups tbb-4 .. tbb-7 -> entries 4-7")
-        e(f"{ind}  const uint32_t xo = (uint32_t)(txa + txs * max(tbb - r, a.b_lo)) * {SQ * NT * 16}u;")
-        e(f"{ind}  uint4* const dst = {self.drain_entry('r')};")
-        for q in range(SQ):
-            e(f"{ind}  vt::cp_async16(dst + {q * NT}, slotc + xo + {q * NT * 16}u, 16, 0);")
+        self.fetch_group(ind + "  ", "tbb - r", self.drain_entry('r'))
         e(f"{ind}  vt::cp_async_commit();")
         e(f"{ind}}}")
         e(f"{ind}int dr = 0;  // drain ring entry of group tbb")
@@ -577,10 +611,7 @@ class Gen16:
             e(f"{ind}    }}")
         e(f"{ind}    --tbb;")
         e(f"{ind}    {{")
-        e(f"{ind}      const uint32_t xo = (uint32_t)(txa + txs * max(tbb - 7, a.b_lo)) * {SQ * NT * 16}u;")
-        e(f"{ind}      uint4* const dst = {self.drain_entry('dr')};")
-        for q in range(SQ):
-            e(f"{ind}      vt::cp_async16(dst + {q * NT}, slotc + xo + {q * NT * 16}u, 16, 0);")
+        self.fetch_group(ind + "      ", "tbb - 7", self.drain_entry('dr'))
         e(f"{ind}      vt::cp_async_commit();")
         e(f"{ind}    }}")
         e(f"{ind}    dr = (dr + 1) & 7;")
@@ -695,10 +726,20 @@ class Gen16:
             for j in range(S):
                 if j not in pre:
                     e(f"{ind}  const uint32_t h{j} = m{j} & {hm:#x}u;")
-        for g in range(S // 16):
-            ws = ", ".join(words[4 * g: 4 * g + 4])
-            pol = ("pol_c" if self.efc else "pol_h") if self.EF else "pol_last"
-            e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), {pol});")
+        pol = ("pol_c" if self.efc else "pol_h") if self.EF else "pol_last"
+        if self.tmh:
+            e(f"{ind}  const uint32_t hwv[16] = {{{', '.join(words)}}};")
+            e(f"{ind}  const int tpos = parity ? (a.nbs - 1 - gs) : gs;")
+            e(f"{ind}  if (tmw && (unsigned)(tpos - tm_p0) < 16u) {{  // warp-uniform: the group goes to TMEM")
+            e(f"{ind}    vt::tc::st16(tm_lane + (uint32_t)(tpos - tm_p0) * 16u, hwv);")
+            e(f"{ind}  }} else {{")
+            for g in range(S // 16):
+                e(f"{ind}    vt::st_global_v4_hint(dst + {g * NT}, make_uint4(hwv[{4 * g}], hwv[{4 * g + 1}], hwv[{4 * g + 2}], hwv[{4 * g + 3}]), {pol});")
+            e(f"{ind}  }}")
+        else:
+            for g in range(S // 16):
+                ws = ", ".join(words[4 * g: 4 * g + 4])
+                e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), {pol});")
         if not self.xmin:  # IMAD clear (FMA pipe): the ALU pipe is the K=7 r1/2 bottleneck
             for j in range(S):
                 e(f"{ind}  m{j} = vt::mad_u32(h{j}, 0xFFFFFFFFu, m{j});")
@@ -747,6 +788,17 @@ class Gen16:
         e("  (void)s_tb;")
         if self.mma:
             self.mma_setup()
+        if self.tmh:
+            e("  // TMEM history window: positions [tm_p0, tm_p0 + 16) of the scratch slot (the middle:")
+            e("  // every position holds an old group in one tile parity and a young one in the other)")
+            e(f"  uint32_t* const tc_tm = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(smem_dyn) + {self.SMEM_TM_OFF});")
+            e("  if (tid < 32) vt::tc::alloc<256>(tc_tm);")
+            e("  vt::tc::fence_before();")
+            e("  __syncthreads();")
+            e("  vt::tc::fence_after();")
+            e("  const uint32_t tm_lane = *tc_tm + ((uint32_t)(32 * (tid >> 5)) << 16);  // this warp's lane quarter")
+            e("  const int tm_p0 = a.nbs >= 16 ? (a.nbs - 16) >> 1 : (1 << 30);")
+            e("  bool tmw = false, tmw_tb = false;  // this warp's groups share one index (this tile / the traced one)")
         if self.polfrac:  # one fractional policy for every history store (no per-group select)
             e(f"  const uint64_t pol_last = VT_POLICY_LAST_FIRST({self.polfrac});")
         else:
@@ -898,6 +950,8 @@ class Gen16:
             e(f"    const int it0 = (int)min(min(max(gA.s - gA.g0, (int64_t)0), max(gB.s - gB.g0, (int64_t)0)) / {P}, "
               f"(int64_t){self.CHB});")
         e("    int it_start = it0;")
+        if self.tmh:
+            e("    tmw = __all_sync(0xFFFFFFFFu, it0 == __shfl_sync(0xFFFFFFFFu, it0, 0));")
         if self.tc:
             e(f"    const int64_t oA0 = oA + (int64_t)it0 * {P * B}, oB0 = oB + (int64_t)it0 * {P * B};")
         e("    // chunks are staged two ahead (cp.async groups): chunk k lives in buffer k & 1")
@@ -1073,6 +1127,9 @@ class Gen16:
         e("    // after the last stores could return stale data (measured: nondeterministic words on")
         e("    // multi-tile launches)")
         e("    __threadfence();")
+        if self.tmh:
+            e("    vt::tc::wait_st();  // this tile's TMEM groups before they are read back")
+            e("    tmw_tb = tmw;")
         for r in range(self.TBD):
             self.tb_fetch("    ", f"tbb - {r}", f"{r}")
         e("  }")
@@ -1093,5 +1150,9 @@ class Gen16:
             e("  vt::tc::fence_before();")
             e("  __syncthreads();")
             e("  if (tid < 32) vt::tc::dealloc<256>(tmb);")
+        if self.tmh:
+            e("  vt::tc::fence_before();")
+            e("  __syncthreads();")
+            e("  if (tid < 32) vt::tc::dealloc<256>(*tc_tm);")
         e("}")
         e("")

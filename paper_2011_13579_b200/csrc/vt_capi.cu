@@ -77,7 +77,7 @@ struct KernelEntry {
   const void* fn;
   const void* fn_nofm;  // variant without final-metric bookkeeping (nullptr: use fn)
   int smem;             // dynamic shared memory bytes per CTA
-  int tc;               // 1: tcgen05 / 2: mma.sync branch-metric variant (opt-in)
+  int tc;               // 1: tcgen05 / 2: mma.sync branch-metric variant (opt-in); 3: TMEM history window
   int nt;               // threads per CTA
   // kernels of a runtime-loaded code module (vt_load_code_module) launch through the module,
   // which carries its own CUDA runtime registration of them
@@ -116,7 +116,7 @@ std::mutex g_dyn_mu;
 // s32 otherwise.  VT_KERNEL_VARIANT forces one.
 int variant_rank(const KernelEntry* e, const char* env) {
   // lower is better; entries of the requested variant win, then the default order
-  const bool is16 = e->WPT > 1, istc = e->tc != 0;
+  const bool is16 = e->WPT > 1, istc = e->tc == 1 || e->tc == 2;  // (tc 3: TMEM history window, a default form)
   if (env && strcmp(env, "16x2tc") == 0) return e->tc == 1 ? 0 : (is16 && !istc ? 1 : 2);
   if (env && strcmp(env, "16x2mma") == 0) return e->tc == 2 ? 0 : (is16 && !istc ? 1 : 2);
   if (env && strcmp(env, "16x2") == 0) return (is16 && !istc) ? 0 : (istc ? 2 : 1);
@@ -197,7 +197,7 @@ int prepare(const KernelEntry* k) {
             k->tc, occ, (int)e, fa.numRegs, fa.sharedSizeBytes, k->smem, fa.maxDynamicSharedSizeBytes);
   }
   if (e != cudaSuccess || occ < 1) occ = 1;
-  if (k->tc == 1 && e == cudaSuccess) {
+  if ((k->tc == 1 || k->tc == 3) && e == cudaSuccess) {
     // The occupancy query answers 1 for the tcgen05 kernels although two CTAs fit (256 TMEM
     // columns each, 2 x ~77 KB shared memory, <= 240 registers): size by those limits.
     cudaFuncAttributes fa;
