@@ -234,11 +234,9 @@ class Gen16:
         # TMEM history window (see tmh_* below): 16 of a tile's stored-group positions live in the
         # CTA's tensor memory (256 columns x 128 lanes: one 16-word group per thread and column
         # block) instead of the HBM scratch slot
-        self.tmh_mode = int(os.environ.get("VT_TMH16", "0"))
-        self.tmh = (self.tmh_mode in (1, 2) and not tc and not mma and self.pbr and NT == 128 and self.S == 64)
-        # mode 2: branch-free store side -- every group is written to TMEM (block 15 is a trash
-        # block for groups outside the 15-position window) and the HBM stores are predicated
-        self.TMW = 15 if self.tmh_mode == 2 else 16
+        self.tmh = (os.environ.get("VT_TMH16", "0") == "1" and not tc and not mma and self.pbr and NT == 128
+                    and self.S == 64)
+        self.TMW = 16
 
         self.polfrac = os.environ.get("VT_POLFRAC16", "")  # e.g. "0.75": fractional evict_last/evict_first
         if self.polfrac:
@@ -733,18 +731,12 @@ class Gen16:
         if self.tmh:
             e(f"{ind}  const uint32_t hwv[16] = {{{', '.join(words)}}};")
             e(f"{ind}  const int tpos = parity ? (a.nbs - 1 - gs) : gs;")
-            if self.tmh_mode == 2:
-                e(f"{ind}  const bool in_tm = tmw && (unsigned)(tpos - tm_p0) < 15u;  // warp-uniform when tmw")
-                e(f"{ind}  vt::tc::st16(tm_lane + (uint32_t)(in_tm ? tpos - tm_p0 : 15) * 16u, hwv);  // block 15: trash")
-                for g in range(S // 16):
-                    e(f"{ind}  if (!in_tm) vt::st_global_v4_hint(dst + {g * NT}, make_uint4(hwv[{4 * g}], hwv[{4 * g + 1}], hwv[{4 * g + 2}], hwv[{4 * g + 3}]), {pol});")
-            else:
-                e(f"{ind}  if (tmw && (unsigned)(tpos - tm_p0) < 16u) {{  // warp-uniform: the group goes to TMEM")
-                e(f"{ind}    vt::tc::st16(tm_lane + (uint32_t)(tpos - tm_p0) * 16u, hwv);")
-                e(f"{ind}  }} else {{")
-                for g in range(S // 16):
-                    e(f"{ind}    vt::st_global_v4_hint(dst + {g * NT}, make_uint4(hwv[{4 * g}], hwv[{4 * g + 1}], hwv[{4 * g + 2}], hwv[{4 * g + 3}]), {pol});")
-                e(f"{ind}  }}")
+            e(f"{ind}  if (tmw && (unsigned)(tpos - tm_p0) < 16u) {{  // warp-uniform: the group goes to TMEM")
+            e(f"{ind}    vt::tc::st16(tm_lane + (uint32_t)(tpos - tm_p0) * 16u, hwv);")
+            e(f"{ind}  }} else {{")
+            for g in range(S // 16):
+                e(f"{ind}    vt::st_global_v4_hint(dst + {g * NT}, make_uint4(hwv[{4 * g}], hwv[{4 * g + 1}], hwv[{4 * g + 2}], hwv[{4 * g + 3}]), {pol});")
+            e(f"{ind}  }}")
         else:
             for g in range(S // 16):
                 ws = ", ".join(words[4 * g: 4 * g + 4])
