@@ -237,6 +237,21 @@ class Gen16:
         self.tmh = (os.environ.get("VT_TMH16", "0") == "1" and not tc and not mma and self.pbr and NT == 128
                     and self.S == 64)
         self.TMW = 16
+        # Alternating cheap/absorbing stages (VT_ALT16=1; the no-final-metric kernel of the cheap
+        # form): body stages C A C A C A instead of N C A N C A -- every even stage is a cheap
+        # stage (one VIADDMNMX per state, metrics leave it offset by -S(p0)), every odd stage
+        # absorbs the offsets through combos.  The renormalisation moves into the absorbing
+        # stages 3 and 5 (a cheap stage cannot fold it), by the minimum over a state set T taken
+        # two stages earlier (after stages 1 and 3, clean values): metrics then stay in
+        # [Sb', Sb' + Delta + 2560 + ...] with Sb' = 256 W_T + 2*dmax (renorm_set with W_T <= 8).
+        self.alt = os.environ.get("VT_ALT16", "0") == "1" and self.cheap and self.B == 2 and not tc and not mma
+        self.alt_now = False
+        if self.alt:
+            r = renorm_set(K, gens, 8)
+            assert r is not None, "alternating form: no renormalisation set"
+            self.alt_T, w_t = r
+            self.Sb_alt = 256 * w_t + 2 * self.dmax
+            assert self.Sb_alt + delta + 2560 + 512 < (1 << (16 - self.L)), "alternating form: metric range"
 
         self.polfrac = os.environ.get("VT_POLFRAC16", "")  # e.g. "0.75": fractional evict_last/evict_first
         if self.polfrac:
@@ -423,11 +438,16 @@ class Gen16:
             e(f"{ind}const uint32_t U{q}_{b} = vt::vadd2(P{q}_{b}, 0x00800080u) << {L};")
             e(f"{ind}const uint32_t N{q}_{b} = {(256 << L) * 0x10001:#x}u - U{q}_{b};")
         outs, body, need_d, need_e = [None] * S, [], set(), set()
+        fw = 1 << gq  # tie-flag weight of this stage
+        is_c = (q % 2 == 0) if self.alt_now else (self.cheap and gq == 1)
+        is_a = (q % 2 == 1) if self.alt_now else (self.cheap and gq == 2)
         ks = list(range(S // 2))
-        if self.seed and not (self.cheap and gq in (1, 2)):
+        # (the interleaved cheap/absorbing pairs keep the natural butterfly order)
+        interleaved = (q in (0, 1, 4, 5)) if self.alt_now else (self.cheap and gq in (1, 2))
+        if self.seed and not interleaved:
             self.rng.shuffle(ks)
         order = [x for k in ks for x in (k, k + S // 2)]
-        if self.cheap and gq == 1:
+        if is_c:
             # CHEAP stage: with the i0 branch metric as a per-state offset phi_j of the
             # stored metric (stored = true - S(p0(j))), the update needs no candidate add:
             #   stored_j = max(m_i1 + T_p0, m_i0),  T_p0 = S(~p0) - S(p0) + 2^1 * flag
@@ -450,15 +470,15 @@ class Gen16:
                     continue
                 pc = p ^ full
                 # per half mod 2^16: T_p = S_pc - S_p + 2f ; T_pc = -T_p + 4f
-                e(f"{ind}const uint32_t T{q}_{p} = vt::vadd2(vt::vadd2(S{q}_{pc}, ~S{q}_{p}), (1u + 2u * {flag}) * 0x10001u);")
-                e(f"{ind}const uint32_t T{q}_{pc} = vt::vadd2(~T{q}_{p}, (1u + 4u * {flag}) * 0x10001u);")
+                e(f"{ind}const uint32_t T{q}_{p} = vt::vadd2(vt::vadd2(S{q}_{pc}, ~S{q}_{p}), (1u + {fw}u * {flag}) * 0x10001u);")
+                e(f"{ind}const uint32_t T{q}_{pc} = vt::vadd2(~T{q}_{p}, (1u + {2 * fw}u * {flag}) * 0x10001u);")
                 done |= {p, pc}
             if defer is not None:
                 defer.extend(body)
             else:
                 self.lines.extend(body)
             return outs
-        if self.cheap and gq == 2:
+        if is_a:
             # offset stage after the cheap one: state i carries phi_i = S1(p0(i)), so the
             # addends are combos S1(class of the predecessor) + S2(branch pattern)
             q1 = q - 1
@@ -479,10 +499,22 @@ class Gen16:
             self.emit_S(ind, q, pb_all)
             for p in sorted({c[1] for c in combos_e}):
                 e(f"{ind}const uint32_t Sf{q}_{p} = S{q}_{p} + {flag} * {(1 << gq) * 0x10001:#x}u;")
-            for pa, pb in sorted(combos_d):
-                e(f"{ind}const uint32_t D{q}_{pa}_{pb} = S{q1}_{pa} + S{q}_{pb};")
-            for pa, pb in sorted(combos_e):
-                e(f"{ind}const uint32_t E{q}_{pa}_{pb} = S{q1}_{pa} + Sf{q}_{pb};")
+            if self.alt_now and q in (3, 5):
+                # renormalisation folded into the combos: -R per half mod 2^16 for the fused
+                # VIADDMNMX operand, as a packed integer for the IMAD operand (see stage())
+                for p in sorted({c[1] for c in combos_d}):
+                    e(f"{ind}const uint32_t SR{q}_{p} = vt::vadd2(S{q}_{p}, negRa{q});")
+                for p in sorted({c[1] for c in combos_e}):
+                    e(f"{ind}const uint32_t SfR{q}_{p} = Sf{q}_{p} + negEa{q};")
+                for pa, pb in sorted(combos_d):
+                    e(f"{ind}const uint32_t D{q}_{pa}_{pb} = vt::vadd2(S{q1}_{pa}, SR{q}_{pb});")
+                for pa, pb in sorted(combos_e):
+                    e(f"{ind}const uint32_t E{q}_{pa}_{pb} = S{q1}_{pa} + SfR{q}_{pb};")
+            else:
+                for pa, pb in sorted(combos_d):
+                    e(f"{ind}const uint32_t D{q}_{pa}_{pb} = S{q1}_{pa} + S{q}_{pb};")
+                for pa, pb in sorted(combos_e):
+                    e(f"{ind}const uint32_t E{q}_{pa}_{pb} = S{q1}_{pa} + Sf{q}_{pb};")
             if defer is not None:
                 # interleave with the deferred cheap stage (all-ALU) so both pipes stay fed:
                 # offset-stage butterfly k and k+S/4 consume cheap butterflies 2k, 2k+1
@@ -520,6 +552,21 @@ class Gen16:
                 e(f"{ind}const uint32_t E{q}_{p} = S{q}_{p} + {k};")
         self.lines.extend(body)
         return outs
+
+    def alt_ref(self, ind: str, q: int, names: list[str]) -> None:
+        """Alternating form: renormalisation reference from the clean outputs of absorbing
+        stage q (the minimum over the state set alt_T), applied two stages later in the
+        absorbing stage q + 2 (negRa / negEa: -R per half mod 2^16 and as a packed integer)."""
+        L = self.L
+        e = self.emit
+        lm = (0xFFFF & ~((1 << L) - 1)) * 0x10001
+        vals = [names[t] for t in self.alt_T]
+        expr = vals[0]
+        for v in vals[1:]:
+            expr = f"vt::vmin2({expr}, {v})"
+        e(f"{ind}const uint32_t ar{q} = ({expr}) & {lm:#x}u;")
+        e(f"{ind}const uint32_t negRa{q + 2} = vt::vadd2(~vt::vadd2(ar{q}, {((-(self.Sb_alt << L)) & 0xFFFF) * 0x10001:#x}u), 0x00010001u);")
+        e(f"{ind}const uint32_t negEa{q + 2} = {(self.Sb_alt << L) * 0x10001:#x}u - ar{q};")
 
     def tma_issue(self, ind: str, k: str) -> None:
         """Lane 0: TMA chunk `k` of the warp's A and B window sets into buffer (k & 1):
@@ -663,8 +710,13 @@ class Gen16:
         if self.fm:
             e(f"{ind}offA += pendA;")
             e(f"{ind}offB += pendB;")
-        e(f"{ind}{{")
-        if self.xmin:  # per-half minimum over all states or over the set rset (history bits masked after)
+        if self.alt_now:
+            e(f"{ind}{{  // (alternating form: renormalised inside the absorbing stages)")
+        else:
+            e(f"{ind}{{")
+        if self.alt_now:
+            pass
+        elif self.xmin:  # per-half minimum over all states or over the set rset (history bits masked after)
             # ternary tree min(min(a, b), c): ptxas fuses each into one VIMNMX3.U16x2
             vals = [f"m{j}" for j in (self.rset if self.rset else range(S))]
             lvl = 0
@@ -687,9 +739,10 @@ class Gen16:
             e(f"{ind}  const uint32_t r0 = {vals[0]} & {lm:#x}u;")
         else:
             e(f"{ind}  const uint32_t r0 = m0 & {lm:#x}u;")
-        e(f"{ind}  const uint32_t rr = vt::vadd2(r0, {((-(self.Sb << L)) & 0xFFFF) * 0x10001:#x}u);")
-        e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);  // -R per half, mod 2^16 (fused-add operand)")
-        e(f"{ind}  negE = {(self.Sb << L) * 0x10001:#x}u - r0;  // -R as a packed integer (IMAD operand)")
+        if not self.alt_now:
+            e(f"{ind}  const uint32_t rr = vt::vadd2(r0, {((-(self.Sb << L)) & 0xFFFF) * 0x10001:#x}u);")
+            e(f"{ind}  negR = vt::vadd2(~rr, 0x00010001u);  // -R per half, mod 2^16 (fused-add operand)")
+            e(f"{ind}  negE = {(self.Sb << L) * 0x10001:#x}u - r0;  // -R as a packed integer (IMAD operand)")
         if self.fm:
             e(f"{ind}  pendA = (int64_t)((r0 & 0xFFFFu) >> {L}) - {self.Sb};")
             e(f"{ind}  pendB = (int64_t)(r0 >> {16 + L}) - {self.Sb};")
@@ -774,6 +827,7 @@ class Gen16:
 
     def kernel_one(self, name: str) -> None:
         K, B, S, L, P, CH, NL, NWC = self.K, self.B, self.S, self.L, self.P, self.CH, self.NL, self.NWC
+        self.alt_now = self.alt and not self.fm  # (the final-metric kernel keeps N C A groups)
         SQ = S // 16  # uint4 of history words per group per thread
         e = self.emit
         targ = ", const __grid_constant__ CUtensorMap tmap" if self.tma else ""
@@ -934,6 +988,8 @@ class Gen16:
             e(f"    const int padA = (int)min(max(gA.s - gA.g0, (int64_t)0), (int64_t){1 << 20}), "
               f"padB = (int)min(max(gB.s - gB.g0, (int64_t)0), (int64_t){1 << 20});")
         m0 = (self.Sb << L) * 0x10001 if self.cheap else 0  # cheap stages need m_i1 + T >= 0 from the start
+        if self.alt_now:
+            m0 = (self.Sb_alt << L) * 0x10001
         e("    " + " ".join(f"uint32_t m{j} = {m0:#x}u;" for j in range(S)))
         e("    uint32_t negR = 0, negE = 0;")
         if self.fm:
@@ -1041,7 +1097,12 @@ class Gen16:
             if q % L == 0:
                 e("        // history codes only in groups whose decisions are stored (warm-up needs none)")
                 e(f"        const uint32_t cflag{q} = (gidx >= a.b_lo) ? 1u : 0u;")
-            names = self.stage("        ", q, names, deferred if (self.cheap and q % L in (1, 2)) else None)
+            # (alternating form: a cheap stage is deferred and interleaved with the absorbing stage
+            # after it only inside a group -- stage 2 ends a group, stage 3 starts one)
+            dq = (q in (0, 1, 4, 5)) if self.alt_now else (self.cheap and q % L in (1, 2))
+            names = self.stage("        ", q, names, deferred if dq else None)
+            if self.alt_now and q in (1, 3):
+                self.alt_ref("        ", q, names)
             if q % L == L - 1:
                 for j in range(S):
                     e(f"        m{j} = {names[j]};")

@@ -6,7 +6,7 @@ instead of the exact minimum, which is safe while min_T Lambda - min Lambda <= 2
 Greedy search over max-magnitude LLR tuples (random tie-breaks, 2-step lookahead) that
 maximises the gap min_T Lambda - min Lambda for the generator's own sets T (both group
 positions of the K=9 body), with the spread as a secondary score.
-usage: python make_adversarial_gap.py [k7r3|k9r2]
+usage: python make_adversarial_gap.py [k7r3|k9r2|k7r2alt]
 Output: tests/golden/adversarial_gap_<code>.npz (int8 (N, B), plus the largest gap seen).
 """
 import itertools
@@ -20,13 +20,18 @@ sys.path.insert(0, os.path.join(HERE, "..", "..", "paper_2011_13579_b200", "csrc
 from gen_kernels16 import Gen16  # noqa: E402
 from gen_kernels16m import Gen16M  # noqa: E402
 
-CODES = {"k7r3": (7, (0o133, 0o171, 0o165)), "k9r2": (9, (0o753, 0o561))}
+CODES = {"k7r3": (7, (0o133, 0o171, 0o165)), "k9r2": (9, (0o753, 0o561)), "k7r2alt": (7, (0o171, 0o133))}
 name = sys.argv[1] if len(sys.argv) > 1 else "k7r3"
 K, G = CODES[name]
 S = 1 << (K - 1)
 if K == 9:
     g = Gen16M(name, K, G, 4)
     sets = [np.array(r[0]) for r in g.rsets]
+elif name.endswith("alt"):  # the alternating form's renormalisation set (VT_ALT16)
+    os.environ["VT_ALT16"] = "1"
+    g = Gen16(name, K, G)
+    sets = [np.array(g.alt_T)]
+    g.Sb = g.Sb_alt
 else:
     g = Gen16(name, K, G)
     sets = [np.array(g.rset)]

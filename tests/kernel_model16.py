@@ -46,6 +46,12 @@ def decode_stream_model16(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> n
     g = _gen(K, gens)
     L, CH, Sb, cheap, xmin = g.L, g.CH, g.Sb, g.cheap, g.xmin
     multilane = hasattr(g, "rsets")
+    # alternating form (VT_ALT16, no-final-metric kernel): body stages C A C A C A, the
+    # renormalisation folded into absorbing stages 3 and 5 from references after stages 1, 3
+    alt = bool(getattr(g, "alt", False))
+    if alt:
+        Sb = g.Sb_alt
+        alt_T = np.array(g.alt_T)
     # renormalisation reference per group position in the body: all states (exact minimum),
     # the subset T (gen_kernels16.renorm_set) or state 0
     if multilane and g.rsets:
@@ -82,6 +88,7 @@ def decode_stream_model16(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> n
         s, stop = max(0, e0 - V), min(n, e1 + V)
         g0 = stop - CH * nc
         m = np.full(S, (Sb << L) if (cheap or multilane) else 0, dtype=np.int64)
+        r_alt = {}
         negR = 0  # renormalisation R = Lambda_ref*2^L - Sb*2^L, subtracted in group stage 0
         fields = {}
         s_prev = None
@@ -93,7 +100,25 @@ def decode_stream_model16(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> n
                 U = (ll + 128) << L
                 N = (256 << L) - U
                 Sp = np.array([sum(int(N[b] if (p >> b) & 1 else U[b]) for b in range(B)) for p in range(1 << B)])
-                if cheap and gq == 1:
+                qb = (gi % g.GPB) * L + gq  # body position
+                if alt and qb % 2 == 0:
+                    T = Sp[p0 ^ full] - Sp[p0] + flag * (1 << gq)
+                    cand1 = m[i1] + T
+                    _in_range(cand1, "cheap candidate")
+                    m = np.maximum(cand1, m[i0])
+                    s_prev = Sp
+                elif alt:
+                    r = r_alt.get(qb, 0) if qb in (3, 5) else 0
+                    d = s_prev[c0] + Sp[p0] - r
+                    e = s_prev[c1] + Sp[p1] + flag * (1 << gq) - r
+                    cand0, cand1 = m[i0] + d, m[i1] + e
+                    _in_range(cand0, "candidate 0")
+                    _in_range(cand1, "candidate 1")
+                    m = np.maximum(cand0, cand1)
+                    if qb in (1, 3):  # reference for the absorbing stage two stages on
+                        lm_ = LIM - (1 << L)
+                        r_alt[qb + 2] = (int(m[alt_T].min()) & lm_) - (Sb << L)
+                elif cheap and gq == 1:
                     T = Sp[p0 ^ full] - Sp[p0] + 2 * flag  # i1 candidate relative to i0's offset
                     cand1 = m[i1] + T
                     _in_range(cand1, "cheap candidate")
@@ -115,13 +140,16 @@ def decode_stream_model16(llr_nb: np.ndarray, K: int, gens, F: int, V: int) -> n
                     m = np.maximum(cand0, cand1)
             # group end: renormalisation reference, fields, clear
             lm = LIM - (1 << L)
-            if refsets is not None:
+            if alt:
+                pass
+            elif refsets is not None:
                 ref = int(m[refsets[gi % g.GPB]].min()) & lm
                 # the subset minimum is within 256 * W_T = Sb of the exact minimum
                 assert int(m.min()) & lm >= ref - (Sb << L)
             else:
                 ref = (int(m.min()) if xmin else int(m[0])) & lm
-            negR = ref - (Sb << L)
+            if not alt:
+                negR = ref - (Sb << L)
             h = m & ((1 << L) - 1)
             if gi >= b_lo:
                 fields[gi] = h.copy()

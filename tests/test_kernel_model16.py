@@ -57,3 +57,31 @@ def test_model16_range_check_has_teeth(monkeypatch):
     q = np.load(os.path.join(ROOT, "tests", "golden", "adversarial_k7r2.npz"))["llr"][:3000]
     with pytest.raises(AssertionError, match="16-bit half"):
         km.decode_stream_model16(q, 7, (0o171, 0o133), 256, 42)
+
+
+@pytest.mark.parametrize("stream", ["adversarial_k7r2", "adversarial_gap_k7r2alt"])
+def test_model16_alternating_form(stream, monkeypatch):
+    """The alternating cheap/absorbing form (VT_ALT16): bit-exact and in range on the
+    max-spread and subset-minimum-gap streams, and on the golden stream cases."""
+    monkeypatch.setenv("VT_ALT16", "1")
+    q = np.load(os.path.join(ROOT, "tests", "golden", f"{stream}.npz"))["llr"][:3000]
+    gens = (0o171, 0o133)
+    want = oracle.decode_stream(q, 7, gens, 256, 42, threads=4)
+    np.testing.assert_array_equal(decode_stream_model16(q, 7, gens, 256, 42), want)
+
+
+def test_model16_alternating_range_check_has_teeth(monkeypatch):
+    """With the alternating form's renormalisation target at 0 instead of 256 * W_T + 2 * dmax
+    the candidates leave the 16-bit half on the gap stream."""
+    import kernel_model16 as km
+    monkeypatch.setenv("VT_ALT16", "1")
+    real = km._gen
+
+    def weak(K, gens):
+        g = real(K, gens)
+        g.Sb_alt = 0
+        return g
+    monkeypatch.setattr(km, "_gen", weak)
+    q = np.load(os.path.join(ROOT, "tests", "golden", "adversarial_gap_k7r2alt.npz"))["llr"][:3000]
+    with pytest.raises(AssertionError, match="16-bit half"):
+        km.decode_stream_model16(q, 7, (0o171, 0o133), 256, 42)
