@@ -36,6 +36,9 @@ import os
 from gen_kernels import parity
 
 NT = int(os.environ.get("VT_NT16", "128"))  # threads per CTA of the 16x2 kernels (2 windows each)
+# (the traceback's ring addressing -- (j & 48) << 7 = (j >> 4) * NT * 16 -- and the TMA boxes are
+# written for 128 threads; VT_NT16=64 measured an illegal address, round 2b)
+assert NT == 128, "the 16x2 kernels are generated for 128-thread CTAs"
 
 CH_BODIES = 2  # loop bodies per LLR chunk
 MINB16 = 1  # CTAs per SM bound (3 forces a 168-register cap: spills, measured 16% slower with the ring traceback)
