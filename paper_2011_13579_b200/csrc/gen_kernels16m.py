@@ -71,6 +71,7 @@ class Gen16M(Gen16):
         # per-lane tree over all 64 slots + 2 xor shuffles.  K=9 (753,561): T = {0, 193} /
         # {0, 4}, W_T = 9 / 10, Sb' = 2560: 2560 + 3328 + 3*512 = 7424 < 8192.
         self.clri = int(os.environ.get("VT_CLRI16M", "32"))  # group end: IMAD clears (see group_end)
+        self.EF = int(os.environ.get("VT_EF16M", "0"))  # evict-first split of the history stores (1/256)
         self.gebf = os.environ.get("VT_GEBF16M", "1") == "1"
         self.rsets = None
         self.GPB = self.P // self.L
@@ -353,6 +354,8 @@ class Gen16M(Gen16):
             words = [f"hw{w}" for w in range(SL // 4)]
         e(f"{ind}if (gidx >= a.b_lo) {{")
         e(f"{ind}  const int gs = gidx - a.b_lo;")
+        if self.EF:
+            e(f"{ind}  const uint64_t pol_h = gs < ef_lim ? pol_first : pol_last;")
         e(f"{ind}  uint4* const dst = slot + (size_t)(parity ? (a.nbs - 1 - gs) : gs) * {SQ} * {NT};")
         if not self.gebf:
             for r in range(SL):
@@ -360,7 +363,7 @@ class Gen16M(Gen16):
                     e(f"{ind}  const uint32_t h{r} = m{r} & {hm:#x}u;")
         for g in range(SQ):
             ws = ", ".join(words[4 * g: 4 * g + 4])
-            e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), pol_last);")
+            e(f"{ind}  vt::st_global_v4_hint(dst + {g * NT}, make_uint4({ws}), {'pol_h' if self.EF else 'pol_last'});")
         e(f"{ind}}}")
         # clear unconditionally (warm-up groups carry no decision bits): no phi moves
         for r in range(SL):
@@ -440,6 +443,9 @@ class Gen16M(Gen16):
         e(f"  const uint32_t* const xr = xw + t * {self.G};")
         e(f"  const char* const rsb = reinterpret_cast<const char*>(s_tb + pair * {T});  // the pair's ring columns")
         e("  const uint64_t pol_last = vt::policy_evict_last();")
+        if self.EF:  # the oldest EF/256 of the stored groups evict-first (as Gen16)
+            e("  const uint64_t pol_first = vt::policy_evict_first();")
+            e(f"  const int ef_lim = (a.nbs * {self.EF}) >> 8;")
         e("  const int64_t nwin = a.w1 - a.w0;")
         e("  const int64_t buf_bytes = (a.st1 - a.st0) * B;")
         e(f"  uint4* const slot = a.scratch + (size_t)blockIdx.x * a.nbs * {SQ} * {NT} + tid;")
