@@ -85,6 +85,11 @@ class Gen:
         self.NL = self.B + 1  # staged 16-byte LLR words per block
         self.NWC = -(-self.BL * self.B // 4)  # realigned LLR words per block
         assert self.NWC + 4 <= 4 * self.NL
+        # shared memory: LLR staging, traceback fields, lane exchange; above the 48 KB of
+        # static shared memory a kernel may declare, the same layout goes dynamic
+        smem = self.NL * NT * 16 + NT * 4 + ((NT // T) * self.XS * 4 if T > 1 else 0)
+        self.dyn_smem = smem > 48 * 1024
+        self.SMEM_DYN = smem if self.dyn_smem else 0
         self.lines: list[str] = []
 
     # -- state <-> (lane, slot) maps for a partition at bits [lo, lo+tau) --------
@@ -215,10 +220,18 @@ class Gen:
         e("  const int tid = threadIdx.x;")
         e(f"  const int t = tid & {T - 1};")
         e(f"  const int wloc = tid >> {tau};")
-        e(f"  __shared__ __align__(16) uint4 s_llr[NL * {NT}];")
-        e(f"  __shared__ uint32_t s_tb[{NT}];")
+        if self.dyn_smem:  # over the 48 KB static limit (e.g. K=8 with three outputs): dynamic
+            e("  extern __shared__ __align__(16) uint4 smem_dyn[];")
+            e("  uint4* const s_llr = smem_dyn;")
+            e(f"  uint32_t* const s_tb = reinterpret_cast<uint32_t*>(smem_dyn + NL * {NT});")
+            if T > 1:
+                e(f"  int32_t* const xs = reinterpret_cast<int32_t*>(s_tb + {NT});")
+        else:
+            e(f"  __shared__ __align__(16) uint4 s_llr[NL * {NT}];")
+            e(f"  __shared__ uint32_t s_tb[{NT}];")
         if T > 1:
-            e(f"  __shared__ __align__(16) int32_t xs[{WPC} * {xstride}];")
+            if not self.dyn_smem:
+                e(f"  __shared__ __align__(16) int32_t xs[{WPC} * {xstride}];")
             e(f"  int32_t* const xw = xs + wloc * {xstride};")
             e(f"  const int32_t* const xr = xw + t * {self.G};")
             e("  const int lane0 = (tid & 31) & ~%d;" % (T - 1))
@@ -398,7 +411,7 @@ def code_units(name: str, K: int, gens: tuple[int, ...]) -> list[tuple[str, str,
     g = Gen(name, K, gens, T)
     units.append((f"vtk_{name}.cu", g.kernel(),
                   [f'extern "C" __global__ void vtk_{name}(const vt::StreamArgs a);'],
-                  [f"VT_KERNEL(vtk_{name}, nullptr, 0, 0, {NT}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, "
+                  [f"VT_KERNEL(vtk_{name}, nullptr, {g.SMEM_DYN}, 0, {NT}, {K}, {len(gens)}, {T}, 1, {g.SL}, {g.BL}, {g.BL}, "
                    f"{g.SQ}, 0, 0, {{{gl}}})"]))
     lanes = T if K in (8, 9) else 0  # (K=7 over 2 lanes measured 97.6 vs 165 Gbps: DESIGN §9b)
     if lanes:  # packed 16x2 variant over T lanes per window pair

@@ -74,7 +74,8 @@ def test_generated_code_batch_matches_reference(vt, z2, case):
 
 
 @pytest.mark.parametrize("k,gens", [(7, (0o133, 0o171)), (5, (0o25, 0o33)), (5, (0o25, 0o33, 0o37, 0o31)),
-                                    (9, (0o557, 0o663, 0o711)), (6, (0o65, 0o57)), (8, (0o345, 0o237))])
+                                    (9, (0o557, 0o663, 0o711)), (6, (0o65, 0o57)), (8, (0o345, 0o237)),
+                                    (8, (0o237, 0o261, 0o313))])  # (K=8 B=3: the s32 form's shared memory goes dynamic)
 @pytest.mark.parametrize("variant", [None, "s32"])
 def test_generated_code_large_stream_vs_oracle(vt, k, gens, variant, monkeypatch):
     """Multi-tile launches of every generated form (16x2 / multi-lane 16x2 / s32) for
