@@ -101,8 +101,9 @@ const KernelEntry* registry(int* n) {
 }
 
 // Kernels of runtime-loaded code modules (vt_load_code_module): appended under a lock,
-// published by the release store of g_ndyn, never removed (entries stay valid).
-constexpr int kMaxDyn = 64;
+// published by the release store of g_ndyn, never removed (entries stay valid).  1024 entries:
+// ~400 distinct run-time codes per process (64 ran out after ~25 codes in tools/stress_codes.py).
+constexpr int kMaxDyn = 1024;
 KernelEntry g_dyn[kMaxDyn];
 std::atomic<int> g_ndyn{0};
 std::mutex g_dyn_mu;
@@ -168,7 +169,7 @@ int validate(const vt_code* c) {
 // Per (kernel entry, device) launch facts, computed once: the dynamic shared memory
 // opt-in (cudaFuncSetAttribute) and the CTA capacity sms * occupancy.  Small calls
 // (one frame) are host-bound, so these stay off the per-call path.
-constexpr int kMaxEntries = 128, kMaxDevices = 64;
+constexpr int kMaxEntries = 64 + kMaxDyn, kMaxDevices = 64;
 std::atomic<int> g_cap[kMaxEntries][kMaxDevices];  // 0: not yet computed
 
 int current_device() {

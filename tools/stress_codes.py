@@ -1,5 +1,5 @@
 """Randomised stress of run-time code modules (jit.py) for arbitrary feed-forward codes:
-random K in {7, 8, 9}, B in {2, 3} generators (top and bottom taps set), each code's kernels
+random K in 3..9, B in 2..4 generators (top and bottom taps set), each code's kernels
 generated and compiled at first use -- the 16x2 forms with their subset-minimum state sets
 chosen per code (gen_kernels16.renorm_set) -- and decoded against the oracle on uniform,
 saturated and AWGN streams with random frame length / overlap.
@@ -19,8 +19,8 @@ rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 t_end = time.time() + float(sys.argv[2] if len(sys.argv) > 2 else 600)
 codes = fails = runs = 0
 while time.time() < t_end:
-    K = int(rng.choice([7, 8, 9]))
-    B = int(rng.choice([2, 2, 3]))
+    K = int(rng.choice([3, 4, 5, 6, 7, 7, 8, 8, 9, 9]))
+    B = int(rng.choice([2, 2, 3, 4]))
     gens = tuple(sorted({int(rng.integers(0, 1 << (K - 2))) << 1 | 1 | (1 << (K - 1)) for _ in range(B)}))
     if len(gens) < B:
         continue
