@@ -419,6 +419,7 @@ def code_units(name: str, K: int, gens: tuple[int, ...]) -> list[tuple[str, str,
         gm = Gen16M(name, K, gens, lanes)
         # the host's padding-skip hazard check (vt_capi.cu launch_grid) uses the body length
         assert gm.CH % gm.P == 0 and gm.P % gm.L == 0
+    if lanes and gm.supported:  # (the s32 kernels alone when the 16-bit range does not fit)
         units.append((f"vtk16m_{name}.cu", gm.kernel(),
                       [f'extern "C" __global__ void vtk16m_{name}(const vt::StreamArgs a);',
                        f'extern "C" __global__ void vtk16mnf_{name}(const vt::StreamArgs a);'],

@@ -90,7 +90,9 @@ class Gen16M(Gen16):
             if all(f is not None for f in found):
                 self.rsets = found
                 self.Sb += 256 * max(f[1] for f in found)
-        assert self.Sb + delta + self.L * 2 * self.dmax < (1 << (16 - self.L)), "metric range"
+        # the 16-bit range must hold (with the exact minimum at worst); codes whose spread does
+        # not fit (e.g. K=9 with three or four outputs) get the s32 kernels only (code_units)
+        self.supported = self.Sb + delta + self.L * 2 * self.dmax < (1 << (16 - self.L))
         self.pbr = True
         self.tc = False
         self.mma = False
