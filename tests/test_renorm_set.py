@@ -71,3 +71,14 @@ def test_compiled_codes_fit_the_16_bit_range():
         assert g.Sb + delta + g.L * 2 * g.dmax < (1 << (16 - g.L)), name
         if getattr(g, "rset", None):
             assert g.Sb == 256 * _w_t(weight_table(K, gens), g.rset, 1 << (K - 1))
+
+
+def test_multilane_form_only_where_the_range_fits():
+    """A K=9 code with four outputs spreads its metrics beyond 16-bit halves: its run-time
+    module carries the s32 kernels alone (it used to assert in the generator)."""
+    from gen_kernels import code_units
+    from gen_kernels16m import Gen16M
+    gens = (0o445, 0o605, 0o621, 0o713)
+    assert not Gen16M("x", 9, gens, 4).supported
+    assert [u[0] for u in code_units("x", 9, gens)] == ["vtk_x.cu"]
+    assert Gen16M("x", 9, (0o557, 0o663, 0o711), 4).supported
