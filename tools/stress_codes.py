@@ -2,7 +2,8 @@
 random K in 3..9, B in 2..4 generators (top and bottom taps set), each code's kernels
 generated and compiled at first use -- the 16x2 forms with their subset-minimum state sets
 chosen per code (gen_kernels16.renorm_set) -- and decoded against the oracle on uniform,
-saturated and AWGN streams with random frame length / overlap.
+saturated and AWGN streams with random frame length / overlap, plus a decode_batch of
+random frames (decoded bits and final metrics).
 usage: python tools/stress_codes.py [seed] [seconds]"""
 import os
 import sys
@@ -46,5 +47,14 @@ while time.time() < t_end:
         if not np.array_equal(got, want):
             fails += 1
             print("FAIL", K, [oct(g) for g in gens], F, V, n, kind, int((got != want).sum()), flush=True)
-    print(f"code K={K} {[oct(g) for g in gens]}: 4 streams ({time.time() - t0:.1f} s incl. JIT)", flush=True)
+    # decode_batch: frames with bits and final metrics (the final-metric kernel variants)
+    nf, nl = int(rng.integers(1, 300)), int(rng.integers(1, 700))
+    fr = rng.integers(-128, 128, size=(nf, B, nl)).astype(np.int8)
+    wb, wm = oracle.decode_batch(fr, K, gens)
+    gb, gm = vt.decode_batch(fr.astype(np.float64), spec)
+    runs += 1
+    if not (np.array_equal(gb, wb) and np.array_equal(gm, wm.astype(np.float64))):
+        fails += 1
+        print("FAIL batch", K, [oct(g) for g in gens], nf, nl, flush=True)
+    print(f"code K={K} {[oct(g) for g in gens]}: 4 streams + a batch ({time.time() - t0:.1f} s incl. JIT)", flush=True)
 print(f"codes {codes} runs {runs} fails {fails}")
