@@ -50,11 +50,23 @@ while time.time() < t_end:
     # decode_batch: frames with bits and final metrics (the final-metric kernel variants)
     nf, nl = int(rng.integers(1, 300)), int(rng.integers(1, 700))
     fr = rng.integers(-128, 128, size=(nf, B, nl)).astype(np.int8)
-    wb, wm = oracle.decode_batch(fr, K, gens)
-    gb, gm = vt.decode_batch(fr.astype(np.float64), spec)
+    mode = "hard" if rng.random() < 0.3 else "soft"
+    ren = bool(rng.random() < 0.3)
+    wb, wm = oracle.decode_batch(fr, K, gens, mode=mode, renormalize=ren)
+    gb, gm = vt.decode_batch(fr.astype(np.float64), spec, mode=mode, renormalize=ren)
     runs += 1
     if not (np.array_equal(gb, wb) and np.array_equal(gm, wm.astype(np.float64))):
         fails += 1
-        print("FAIL batch", K, [oct(g) for g in gens], nf, nl, flush=True)
+        print("FAIL batch", K, [oct(g) for g in gens], nf, nl, mode, ren, flush=True)
+    # decode_reference with non-uniform initial metrics (the forward/traceback kernels)
+    S = 1 << (K - 1)
+    init = rng.integers(-3000, 3000, size=S)
+    fr1 = rng.integers(-128, 128, size=(B, int(rng.integers(1, 400)))).astype(np.int8)
+    wb1, _ = oracle.decode_frame(fr1, K, gens, initial_metrics=init, renormalize=ren)
+    gb1 = vt.decode_reference(fr1.astype(np.float64), spec, initial_metrics=init.astype(np.float64), renormalize=ren)
+    runs += 1
+    if not np.array_equal(np.asarray(gb1, dtype=np.uint8), wb1):
+        fails += 1
+        print("FAIL reference", K, [oct(g) for g in gens], fr1.shape, ren, flush=True)
     print(f"code K={K} {[oct(g) for g in gens]}: 4 streams + a batch ({time.time() - t0:.1f} s incl. JIT)", flush=True)
 print(f"codes {codes} runs {runs} fails {fails}")
