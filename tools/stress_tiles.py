@@ -46,7 +46,8 @@ while time.time() < t_end:
     ok = np.array_equal(res.bits, wb) and np.array_equal(res.final_metric, wm, equal_nan=True)
     if radix == 2 and not half:
         ob, om = oracle.decode_batch(llr.astype(np.int64), K, gens, renormalize=ren)
-        ok = ok and np.array_equal(res.bits, ob) and np.array_equal(res.final_metric, om.astype(np.float64))
+        # (decode_batch reports the renormalised final metric, decode_matrix_batch max + offsets)
+        ok = ok and np.array_equal(res.bits, ob) and (ren or np.array_equal(res.final_metric, om.astype(np.float64)))
     if not ok:
         fails += 1
         print("FAIL", K, [oct(g) for g in gens], radix, optimized, half, ren, f, n, flush=True)
