@@ -47,6 +47,14 @@ while time.time() < t_end:
         if not np.array_equal(got, want):
             fails += 1
             print("FAIL", K, [oct(g) for g in gens], F, V, n, kind, int((got != want).sum()), flush=True)
+        if trial == 3:  # the pipelined host entry, two shards on this device (devices=[0, 0])
+            hb = vt.decode_stream_host(torch.from_numpy(q).pin_memory(), spec, F, V,
+                                       nchunks=int(rng.integers(1, 6)), devices=[0, 0])
+            gh = np.unpackbits(hb.numpy().view(np.uint8), count=n, bitorder="little")
+            runs += 1
+            if not np.array_equal(gh, want):
+                fails += 1
+                print("FAIL host", K, [oct(g) for g in gens], F, V, n, flush=True)
     # decode_batch: frames with bits and final metrics (the final-metric kernel variants)
     nf, nl = int(rng.integers(1, 300)), int(rng.integers(1, 700))
     fr = rng.integers(-128, 128, size=(nf, B, nl)).astype(np.int8)
