@@ -36,9 +36,15 @@ import os
 from gen_kernels import parity
 
 NT = int(os.environ.get("VT_NT16", "128"))  # threads per CTA of the 16x2 kernels (2 windows each)
-# (the traceback's ring addressing -- (j & 48) << 7 = (j >> 4) * NT * 16 -- and the TMA boxes are
-# written for 128 threads; VT_NT16=64 measured an illegal address, round 2b)
-assert NT == 128, "the 16x2 kernels are generated for 128-thread CTAs"
+# (the traceback's ring addressing is (j & 48) << log2(NT) = (j >> 4) * NT * 16; VT_NT16=64 measured
+# an illegal address in round 2b, 256 -- one CTA per SM -- is the lockstep experiment below)
+assert NT in (128, 256), "the 16x2 kernels are generated for 128- or 256-thread CTAs"
+NTS = NT.bit_length() - 1
+# VT_LOCK16 (with VT_NT16=256): a barrier after every LLR chunk keeps the two warps of each SM
+# sub-partition (warps w and w + 4) at the same point of the 22.6 KB loop body, so one warp's
+# instruction-cache fills serve the other (no L0 reuse otherwise).  1: a named
+# barrier per warp pair, 2: the whole CTA
+LOCK = int(os.environ.get("VT_LOCK16", "0"))
 
 CH_BODIES = 2  # loop bodies per LLR chunk
 MINB16 = 1  # CTAs per SM bound (3 forces a 168-register cap: spills, measured 16% slower with the ring traceback)
@@ -653,7 +659,7 @@ class Gen16:
         for w, side in (("A", 0), ("B", 16)):
             e(f"{ind}    {{")
             e(f"{ind}      const uint32_t j = tb{w}.j;")
-            e(f"{ind}      const uint32_t wd = *reinterpret_cast<const uint32_t*>(rs + ((j & 48u) << 7) + (j & 12u));")
+            e(f"{ind}      const uint32_t wd = *reinterpret_cast<const uint32_t*>(rs + ((j & 48u) << {NTS}) + (j & 12u));")
             e(f"{ind}      const uint32_t h = (wd >> ((j & 3u) * {L}u + {side}u)) & {fm}u;")
             e(f"{ind}      tb{w}.acc = (tb{w}.acc << {L}) | (j >> {self.k - L});")
             e(f"{ind}      tb{w}.j = ((j << {L}) | h) & {S - 1}u;")
@@ -688,7 +694,7 @@ class Gen16:
         for w, side in (("A", 0), ("B", 16)):
             e(f"{ind}  {{")
             e(f"{ind}    const uint32_t j = tb{w}.j;")
-            e(f"{ind}    const uint32_t wd = *reinterpret_cast<const uint32_t*>(rs + ((j & 48u) << 7) + (j & 12u));")
+            e(f"{ind}    const uint32_t wd = *reinterpret_cast<const uint32_t*>(rs + ((j & 48u) << {NTS}) + (j & 12u));")
             e(f"{ind}    const uint32_t h = (wd >> ((j & 3u) * {L}u + {side}u)) & {fm}u;")
             e(f"{ind}    tb{w}.acc = (tb{w}.acc << {L}) | (j >> {self.k - L});")
             e(f"{ind}    tb{w}.j = ((j << {L}) | h) & {S - 1}u;")
@@ -1119,6 +1125,10 @@ class Gen16:
             e(f"        if (it == {self.CHB // 2 - 1}) {{ tbA.settle(a); tbB.settle(a); }}")
         e("      }")
         e("      it_start = 0;")
+        if LOCK == 1 and NT == 256 and not (self.tc or self.mma or self.tmh):
+            e(f"      asm volatile(\"bar.sync %0, 64;\" :: \"r\"(1 + (warp & 3)) : \"memory\");  // VT_LOCK16: warp pair lockstep")
+        elif LOCK == 2 and NT == 256 and not (self.tc or self.mma or self.tmh):
+            e("      __syncthreads();  // VT_LOCK16=2: CTA lockstep")
         e("      tbA.settle(a);  // whole words of the previous tile's traceback")
         e("      tbB.settle(a);")
         if self.tc:
