@@ -196,3 +196,24 @@ def test_tile_tables_model_matches_reference(z2, case):
     np.testing.assert_array_equal(bits, z2[case["key"] + "_bits"])
     np.testing.assert_array_equal(metric, z2[case["key"] + "_metric"])
     assert ops == int(z2[case["key"] + "_counter"][0])
+
+
+@pytest.mark.parametrize("lock", ["1", "2"])
+def test_lockstep_generator_knob_emits_barriers(lock):
+    """VT_NT16=256 + VT_LOCK16 (the measured-and-rejected warp-pair lockstep form)
+    still generates: 256-thread launch bounds, the NT-scaled traceback ring addressing and one
+    barrier per LLR chunk; the default (128 threads) has neither."""
+    import subprocess
+    import sys
+
+    csrc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2011_13579_b200", "csrc")
+    prog = ("import gen_kernels16 as g; k = g.Gen16('vtk16_k7r2', 7, (0o171, 0o133)); print(k.kernel())")
+    env = dict(os.environ, VT_NT16="256", VT_LOCK16=lock)
+    src = subprocess.run([sys.executable, "-c", prog], cwd=csrc, env=env, capture_output=True, text=True,
+                         check=True).stdout
+    assert "__launch_bounds__(256, 1)" in src and "((j & 48u) << 8)" in src
+    assert ("bar.sync %0, 64;" in src) if lock == "1" else ("__syncthreads();  // VT_LOCK16=2" in src)
+    env = {k: v for k, v in os.environ.items() if k not in ("VT_NT16", "VT_LOCK16")}
+    src = subprocess.run([sys.executable, "-c", prog], cwd=csrc, env=env, capture_output=True, text=True,
+                         check=True).stdout
+    assert "__launch_bounds__(128, 1)" in src and "((j & 48u) << 7)" in src and "VT_LOCK16" not in src
