@@ -36,9 +36,10 @@ import os
 from gen_kernels import parity
 
 NT = int(os.environ.get("VT_NT16", "128"))  # threads per CTA of the 16x2 kernels (2 windows each)
-# (the traceback's ring addressing is (j & 48) << log2(NT) = (j >> 4) * NT * 16; VT_NT16=64 measured
-# an illegal address in round 2b, 256 -- one CTA per SM -- is the lockstep experiment below)
-assert NT in (128, 256), "the 16x2 kernels are generated for 128- or 256-thread CTAs"
+# (the traceback's ring addressing is (j & 48) << log2(NT) = (j >> 4) * NT * 16; it was hard-coded for
+# 128 threads until round 2d, which is why VT_NT16=64 faulted in round 2b.  Measured in round 2d:
+# 64 -> 165.9, 256 -> 162.5 vs 167.3 Gbps, bits identical)
+assert NT in (64, 128, 256), "the 16x2 kernels are generated for 64-, 128- or 256-thread CTAs"
 NTS = NT.bit_length() - 1
 # VT_LOCK16 (with VT_NT16=256): a barrier after every LLR chunk keeps the two warps of each SM
 # sub-partition (warps w and w + 4) at the same point of the 22.6 KB loop body, so one warp's
