@@ -300,7 +300,7 @@ def run_ours(args) -> None:
             "clocks": clocks,
             "ber": {"errors": ber_err, "bits": n, "ber": ber_err / n},
         }
-        if not args.no_other_configs:
+        if not args.no_other_configs and ws == 1:  # (N > 1: the headline only, symmetric teardown)
             line["other_configs"] = other_configs(torch, vt, dev, steps=20)
         if not args.no_cpu_baseline and ws == 1:
             line["cpu_baseline"] = cpu_baseline_full(q_host, decoded, n)
