@@ -23,7 +23,10 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v
 
 def _compile(src: str) -> tuple[str, str]:
     obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
-    if os.path.exists(obj) and os.path.getmtime(obj) >= max(
+    stamp = obj + ".flags"  # the compile flags of the cached object (VT_EXTRA_NVCC changes force a rebuild)
+    flags = " ".join(ARCH + FLAGS)
+    same_flags = os.path.exists(stamp) and open(stamp).read() == flags
+    if same_flags and os.path.exists(obj) and os.path.getmtime(obj) >= max(
             os.path.getmtime(src), *[os.path.getmtime(h) for h in glob.glob(os.path.join(CSRC, "*.cuh"))],
             *[os.path.getmtime(h) for h in glob.glob(os.path.join(CSRC, "gen", "*.inc"))],
             os.path.getmtime(os.path.join(HERE, "..", "include", "vitertile_b200.h"))):
@@ -32,6 +35,8 @@ def _compile(src: str) -> tuple[str, str]:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    with open(stamp, "w") as fh:
+        fh.write(flags)
     return obj, r.stderr
 
 
